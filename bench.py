@@ -1,0 +1,372 @@
+"""Benchmark of the batched candidate-mapping evaluator (driver contract).
+
+Workload (BASELINE.json north star): the 200-node randomly wired
+Watts-Strogatz graph `gen_module("ws", 200, seed=0, k=4, p=0.75)` with
+`synth_profile(DEFAULT3, seed=0)` (V=202, E=457, K=3, L=1), frozen from the
+reference's own generator in tests/golden/instances/ws200.json. A step is one
+pass of the evaluator over a batch of N synthetic uint8 candidate mappings
+(explicit genomes resident in HBM, N*204 B >> 126 MB L2, so no L2 flush is
+needed), producing every makespan plus the fused first-index argmin; with
+--gpus > 1 each rank evaluates its own N (weak scaling) and the global best
+(cost, index) is combined with one NCCL all-gather of 16 B per rank.
+
+`e2e` is the same metric through the public C ABI call with HOST buffers
+(hs_eval_host: pinned genomes in, makespans + best out, copies inside the
+timed region). `cpu_baseline` / `--impl reference` time the CPU oracle port
+of the reference decoder (oracle/hs_oracle.py, a restatement of
+heuristics.py:43-148) on the host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "ws200"
+METRIC = "candidate mappings scored/sec"
+UNIT = "candidates/s"
+
+
+def _load_doc():
+    with open(os.path.join(ROOT, "tests", "golden", "instances",
+                           WORKLOAD + ".json")) as f:
+        return json.load(f)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _config(n, world):
+    return {"workload": "ws200: gen_module('ws',200,seed=0,k=4,p=0.75) + "
+                        "synth_profile(DEFAULT3,seed=0), V=202 E=457 K=3 L=1",
+            "candidates_per_gpu_per_step": n,
+            "genome_layout": "uint8 [N x 204] row-major (sorted-device index "
+                             "per BFS position)",
+            "l2": "inputs larger than L2 (N*204 B >> 126 MB); no flush",
+            "parallelism": f"dp{world} (candidate shards, NCCL 16 B best "
+                           "all-gather)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU legs
+def _cpu_worker(args):
+    doc, lo, hi, seed = args
+    import numpy as np
+    from oracle import hs_oracle as O
+    tb = O.build_tables(O.Instance.from_doc(doc), 1)
+    genes = np.random.default_rng(seed).integers(3, size=(hi - lo, tb.V),
+                                                 dtype=np.uint8)
+    t0 = time.perf_counter()
+    for r in range(hi - lo):
+        O.fitness_one(tb, genes[r])
+    return hi - lo, time.perf_counter() - t0
+
+
+def cpu_port_rate(doc, seconds=12.0, cores=None):
+    """Oracle port of the reference decoder (pure Python, per candidate, the
+    reference's algorithm) on all host cores, bounded sample."""
+    import multiprocessing as mp
+    cores = cores or len(os.sched_getaffinity(0))
+    per = max(50, int(1500 * seconds))  # the port runs ~1500 cand/s/core
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, [(doc, 0, per, 1000 + k)
+                                     for k in range(cores)])
+    wall = time.perf_counter() - t0
+    total = sum(r[0] for r in res)
+    return {"value": total / wall, "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": f"{total} uniform WS200 genomes ({per}/core), "
+                      "oracle/hs_oracle.py fitness_one (pure-Python "
+                      "restatement of heuristics.py:43-148), "
+                      f"multiprocessing fork x{cores}, {wall:.1f} s wall"}
+
+
+def c_port_rate(doc, cores):
+    import numpy as np
+    from oracle import hs_oracle as O
+    from oracle.hs_oracle_c import CTables, load
+    tb = O.build_tables(O.Instance.from_doc(doc), 1)
+    ct, lib = CTables(tb), load()
+    genes = np.random.default_rng(5).integers(3, size=(400_000, tb.V),
+                                              dtype=np.uint8)
+    t0 = time.perf_counter()
+    ct.fitness(lib, genes, cores)
+    return len(genes) / (time.perf_counter() - t0)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    doc = _load_doc()
+    cores = len(os.sched_getaffinity(0))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_port_rate(doc, seconds=max(2.0, 20.0 / (args.steps + 1)),
+                          cores=cores)
+        if s >= args.warmup:
+            vals.append(r)
+    v = statistics.mean(x["value"] for x in vals)
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": None, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": _config(None, 1),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores,
+                            "kind": "port", "sample": vals[-1]["sample"]},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 24,
+                    help="candidates per GPU per step")
+    ap.add_argument("--e2e-n", type=int, default=1 << 23)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2308_00127_b200 as hs
+    from paper_2308_00127_b200 import _native as N
+    from paper_2308_00127_b200.plan import get_plan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    doc = _load_doc()
+    g, hw, table = hs.load_instance(doc)
+    plan = get_plan(g, hw, table, 1)
+    V, ld, n = plan.V, plan.pref_ld, args.n
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1234 + rank)
+    genes = torch.randint(0, plan.K, (n, ld), dtype=torch.uint8,
+                          device="cuda", generator=gen)
+    ms = torch.empty(n, dtype=torch.float64, device="cuda")
+    best = torch.empty(2, dtype=torch.int64, device="cuda")
+    gathered = torch.empty(2 * world, dtype=torch.int64, device="cuda")
+
+    def step():
+        plan.eval(genes, ms, None, best, index_base=rank * n, stream=stream)
+        if dist is not None:
+            dist.all_gather_into_tensor(gathered, best)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), \
+        torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            plan.eval(genes, ms, None, best, index_base=rank * n,
+                      stream=stream)
+            evs[k][1].record(stream)
+            if dist is not None:
+                dist.all_gather_into_tensor(gathered, best)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    if dist is not None:
+        tt = torch.tensor([total_ms, kern_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, kern_ms = float(tt[0]), float(tt[1])
+        gb = gathered.view(world, 2).cpu()
+        cands = [(float(gb[r, :1].view(torch.float64).item()),
+                  int(gb[r, 1].item())) for r in range(world)]
+        bcost, bidx = min(cands)
+    else:
+        b = best.cpu()
+        bcost, bidx = float(b[:1].view(torch.float64).item()), int(b[1].item())
+    ms_step = total_ms / args.steps
+    value = world * n / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (eval_kernel)
+    peak, peak_kind = _peaks()
+    alg_bytes = n * (V + 8)
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "eval_kernel_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                tp = json.load(f)
+            traffic = tp.get("dram_bytes_per_candidate")
+            if traffic is not None:
+                traffic = traffic * n
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C ABI with host buffers (pinned)
+    e2e = None
+    if rank == 0 or world > 1:
+        ne = min(args.e2e_n, n)
+        hg = torch.empty((ne, ld), dtype=torch.uint8, pin_memory=True)
+        hg.copy_(genes[:ne].cpu())
+        hm = torch.empty(ne, dtype=torch.float64, pin_memory=True)
+        hb = N.Best()
+        hgn, hmn = hg.numpy(), hm.numpy()
+        for _ in range(2):
+            plan.eval_host(hgn, hmn, None, hb, stream=stream)
+        torch.cuda.synchronize()
+        reps = max(2, min(args.steps, 5))
+        w0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), \
+            torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            plan.eval_host(hgn, hmn, None, hb, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) / reps
+        dev = e0.elapsed_time(e1) / 1e3 / reps
+        el = max(wall, dev)
+        if dist is not None:
+            tt = torch.tensor([el], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt[0])
+        # parity of the e2e result with the device path on the same genomes
+        assert np.array_equal(hmn, ms[:ne].cpu().numpy())
+        e2e = {"value": world * ne / el, "unit": UNIT,
+               "h2d_bytes_per_step": ne * ld,
+               "d2h_bytes_per_step": ne * 8 + 16,
+               "candidates_per_step": ne, "api": "hs_eval_host (C ABI, "
+               "pinned host genomes, chunked H2D/kernel/D2H on 2 streams)"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        cpu = cpu_port_rate(doc, seconds=10.0, cores=cores)
+        try:
+            cpu["c_port_all_cores"] = c_port_rate(doc, cores)
+        except Exception:
+            pass
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (uniform random genomes; "
+                                "reference benchgen graph frozen as JSON)",
+        "config": _config(n, world),
+        "best": {"cost_ms": bcost, "index": bidx},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "peak_kind": peak_kind, "traffic": traffic,
+                     "algorithmic_bytes_per_candidate": V + 8,
+                     "kernel_ms": kern_ms, "kernel": "hs::eval_kernel"},
+        "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

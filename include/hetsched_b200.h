@@ -1,0 +1,173 @@
+/*
+ * hetsched_b200.h -- C ABI of the B200-native candidate-mapping evaluator.
+ *
+ * Drop-in boundary for the data-parallel hot path of the DiviML reference
+ * (`hetsched`, /root/reference/pkg/src/hetsched). Every entry point takes
+ * plain pointers and sizes (no torch or Python types), is thread-safe (the
+ * reference's ModuleSolver may be called from a thread pool,
+ * splitting.py:342-344), and runs its device work on the caller's stream.
+ * Device pointers are marked d_, host pointers h_.
+ *
+ * Reference interface each entry point replaces:
+ *   hs_plan_create  -- per-call setup inside decode(): sorted(hw.devices)
+ *                      heuristics.py:132, _ListScheduler heuristics.py:46-58,
+ *                      bfs_topological_order core.py:82-101, comm_time
+ *                      core.py:148-155, LatencyTable.get core.py:166-170,
+ *                      _mem_extra heuristics.py:60-65.
+ *   hs_eval         -- fitness(genome, g, hw, table, L) heuristics.py:146-148
+ *                      (decode heuristics.py:127-143) over a batch.
+ *   hs_eval_host    -- same, host buffers in/out (the e2e call a binding
+ *                      makes; H2D / D2H inside).
+ *   hs_eval_gen     -- the candidate draws of the search loops
+ *                      (heuristics.py:276-283, 322-325) fused with fitness.
+ *   hs_trace        -- decode() heuristics.py:127-143 returning the per-task
+ *                      start times that rebuild the Schedule.
+ *   hs_cp_bound     -- critical_path_bound bounds.py:57-72, batched masks.
+ *   hs_reach        -- dep_subgraph / pre_subgraph bounds.py:29-54 and
+ *                      transitive_closure core.py:104-111 as bitsets.
+ *   hs_best_merge   -- (no reference counterpart) lexicographic
+ *                      (cost, index) merge of per-rank bests.
+ */
+#ifndef HETSCHED_B200_H
+#define HETSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+
+/* return codes */
+#define HS_OK 0
+#define HS_EINVAL 1   /* -> hetsched GraphError (bad description, bad gene) */
+#define HS_ECYCLE 2   /* -> GraphError("cycle detected"), core.py:94-95   */
+#define HS_ECUDA 3    /* -> RuntimeError                                   */
+#define HS_ENOMEM 4   /* -> MemoryError                                    */
+
+/* per-candidate status (hs_eval*, hs_trace) */
+#define HS_ST_OK 0        /* feasible: makespan finite or +inf by latency */
+#define HS_ST_BATCH 1     /* unsupported full-batch size heuristics.py:96 */
+#define HS_ST_MEMORY 2    /* capacity exceeded heuristics.py:98-100       */
+#define HS_ST_LINK 3      /* missing link core.py:153-154                 */
+#define HS_ST_MISSING 4   /* missing latency entry: GraphError core.py:169 */
+#define HS_ST_GENE 5      /* gene out of range: GraphError heuristics.py:133 */
+
+typedef struct hs_plan hs_plan; /* opaque, immutable after creation */
+
+/* Instance description, reference wire model (core.py:25-179). Strings are
+ * UTF-8 bytes concatenated with [n+1] offsets; indices refer to insertion
+ * order (tasks dict order, edges list order, devices dict order). */
+typedef struct hs_instance_desc {
+    int32_t n_tasks;
+    const char *task_ids;
+    const int64_t *task_id_off;   /* [n_tasks+1] */
+    const double *wm, *im, *om;   /* [n_tasks] bytes */
+    int32_t n_edges;
+    const int32_t *edge_src;      /* [n_edges] task index */
+    const int32_t *edge_dst;      /* [n_edges] task index */
+    int32_t n_devices;
+    const char *dev_ids;
+    const int64_t *dev_id_off;    /* [n_devices+1] */
+    const double *memory;         /* [n_devices] bytes */
+    const int32_t *batch_off;     /* [n_devices+1] into batch_sizes */
+    const int32_t *batch_sizes;   /* ascending per device */
+    const double *bandwidth;      /* [n_devices^2] beta(a->b) bytes/ms; <=0 = no link */
+    int32_t L;                    /* inputs per task batch (decode's L) */
+    const double *latency;        /* [n_tasks x n_cols], col j = (device, batch) pairs
+                                     enumerated device-major in insertion order,
+                                     batch sizes ascending: table.get(task, dev, b) */
+    const uint8_t *latency_ok;    /* [n_tasks x n_cols] 1 = entry present */
+    const int32_t *order;         /* optional [n_tasks] genome order (task index per
+                                     position); NULL = bfs_topological_order */
+} hs_instance_desc;
+
+typedef struct hs_plan_info {
+    int32_t V, E, K, L;
+    int32_t live_slots;           /* max live end-times per candidate */
+    int32_t n_classes;            /* distinct link bandwidths (comm classes) */
+    int32_t uniform_comm;         /* full mesh, one bandwidth */
+    int32_t full_mesh;
+    int32_t mem_check;            /* 0 = capacity provably never binds */
+    int32_t all_batch_ok;         /* every device supports L */
+    int32_t latency_complete;     /* every needed (task, dev, L) present */
+    int32_t words;                /* ceil(n_tasks/64) for masks / bitsets */
+    int32_t pref_ld;              /* genome row stride that makes the staged
+                                     tile bank-conflict free (>= V) */
+} hs_plan_info;
+
+typedef struct hs_best {
+    double cost;                  /* makespan (ms); +inf if none feasible */
+    int64_t index;                /* global candidate index, first minimum */
+} hs_best;
+
+/* thread-local message of the last failure in this thread */
+const char *hs_last_error(void);
+int hs_abi_version(void);
+
+int hs_plan_create(const hs_instance_desc *desc, hs_plan **out);
+void hs_plan_destroy(hs_plan *plan);
+int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
+/* genome order (task index per position) and sorted device order */
+int hs_plan_order(const hs_plan *plan, int32_t *order, int32_t *dev_order);
+
+/* Batch fitness. d_genes: uint8 [n x ld] row-major, gene = sorted-device
+ * index per genome position. Outputs (each may be NULL): d_makespan f64[n]
+ * (+inf when infeasible, NaN on status >= 4), d_status u8[n], d_best =
+ * first-index argmin with indices offset by index_base. */
+int hs_eval(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
+            double *d_makespan, uint8_t *d_status, hs_best *d_best,
+            int64_t index_base, void *stream);
+
+/* Same with host buffers; h_genes should be pinned for full PCIe rate.
+ * Copies are chunked and overlapped with the kernels on `stream`; returns
+ * after the results are in host memory. */
+int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
+                 int64_t ld, double *h_makespan, uint8_t *h_status,
+                 hs_best *h_best, int64_t index_base, void *stream);
+
+/* On-device candidates: candidate c in [first, first+n) has genes
+ * oracle/hs_oracle.py::gen_genes(seed, c). Optional d_genes_out [n x V]. */
+int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,
+                double *d_makespan, uint8_t *d_status, uint8_t *d_genes_out,
+                hs_best *d_best, void *stream);
+
+/* Generated candidates over genome groups. Position i takes the fixed gene
+ * d_template[i] when d_group[i] < 0, else the value of group d_group[i]
+ * (groups numbered by first position, so d_group[i] <= i); NULL template and
+ * group map = one group per position. HS_GEN_RANDOM: group values of
+ * candidate c are gen_genes(seed, c) over n_groups; HS_GEN_ENUM: group j is
+ * digit j of c in base K (requires first + n <= K^n_groups). Used for the
+ * pinned / co-located module sweeps of the split heuristic's ModuleSolver
+ * (splitting.py:225-245, pins and same_device of milp.py:277-291). */
+#define HS_GEN_RANDOM 1
+#define HS_GEN_ENUM 2
+int hs_eval_gen_ex(const hs_plan *plan, int mode, uint64_t seed, int64_t first,
+                   int64_t n, const uint8_t *d_template, const int16_t *d_group,
+                   int32_t n_groups, double *d_makespan, uint8_t *d_status,
+                   uint8_t *d_genes_out, hs_best *d_best, void *stream);
+
+/* decode(): per-position start times d_start f64[n x V] (row per genome). */
+int hs_trace(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
+             double *d_start, double *d_makespan, uint8_t *d_status,
+             void *stream);
+
+/* critical_path_bound over nsub task masks (bit t = task insertion index t,
+ * words = ceil(n_tasks/64) per mask). d_status[k] = 1 when a task of the
+ * mask lacks a latency entry (GraphError). */
+int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,
+                double *d_out, uint8_t *d_status, void *stream);
+
+/* Descendant / ancestor bitsets [n_tasks x words] (task insertion index). */
+int hs_reach(const hs_plan *plan, uint64_t *d_desc, uint64_t *d_anc,
+             void *stream);
+
+/* host: lexicographic (cost, index) minimum of n bests */
+int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETSCHED_B200_H */

@@ -1,0 +1,25 @@
+"""B200-native batched evaluation of candidate device mappings for DNN task
+graphs (the data-parallel hot path of DiviML, arXiv 2308.00127).
+
+The public surface mirrors the reference package ``hetsched``: data model
+(``core``), decoder and heuristics (``heuristics``), lower bound
+(``bounds``) and the split heuristic's module solver (``splitting``). The
+compute runs in hand-written sm_100a CUDA kernels behind the C ABI of
+``include/hetsched_b200.h`` (``libhetsched_b200.so``); there is no CPU
+fallback.
+"""
+from .core import (Device, DnnGraph, GraphError, HardwareSystem,
+                   LatencyTable, Schedule, ScheduledBatch, ScheduleError,
+                   TaskNode, bfs_topological_order, load_graph, load_hardware,
+                   load_instance, load_latency, load_schedule, save_graph,
+                   save_hardware, save_latency, save_schedule,
+                   transitive_closure)
+from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
+                         fitness, fitness_batch, genome_from_map, greedy, met,
+                         one_plus_one_ea, random_search, simulated_annealing,
+                         throughput)
+from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
+                     dep_subgraph, lower_bound, pre_subgraph)
+from .splitting import ModuleSolver, gpu_module_solver
+
+__version__ = "0.1.0"

@@ -1,0 +1,463 @@
+// extern "C" boundary (include/hetsched_b200.h): argument checking, device
+// state (launch configuration + plan upload per device), scratch, and the
+// host-buffer pipeline. All device work is issued on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+struct hs_plan {
+    hs::Plan p;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char *what) {
+    return set_err(HS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                          \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_err(e_, #call); \
+    } while (0)
+
+int kt_of(int K) { return K <= 2 ? 2 : (K <= 4 ? K : 0); }
+
+uint32_t flags_of(const hs::Plan &p) {
+    uint32_t f = 0;
+    if (p.mem_check) f |= hs::F_MEM;
+    if (!p.all_batch_ok) f |= hs::F_OKL;
+    if (!p.latency_complete) f |= hs::F_MISS;
+    if (p.nan_possible) f |= hs::F_NAN;
+    return f;
+}
+
+}  // namespace
+
+namespace hs {
+
+Plan::~Plan() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (DevState *d : devs) {
+        if (!d) continue;
+        if (d->blob) {
+            cudaSetDevice(d->device);
+            cudaFree(d->blob);
+        }
+        delete d;
+    }
+    if (cur >= 0) cudaSetDevice(cur);
+}
+
+int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        if (err) *err = std::string("cudaGetDevice: ") + cudaGetErrorString(e);
+        return HS_ECUDA;
+    }
+    std::lock_guard<std::mutex> lk(p.mu);
+    if ((int)p.devs.size() > dev && p.devs[dev]) {
+        *out = p.devs[dev];
+        return HS_OK;
+    }
+    int optin = 0, sms = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    DevState *ds = new DevState();
+    ds->device = dev;
+    ds->sms = sms;
+    ds->kt = kt_of(p.K);
+    ds->ld_cap = p.pref_ld() + 16;
+    const bool cls = !p.uniform_comm;
+    const int64_t per_lane = ds->ld_cap + int64_t(p.live_slots) * 8 +
+                             (ds->kt == 0 ? int64_t(16) * p.K : 0);
+    const int64_t budget = int64_t(optin) - 16 - 1024;
+    auto lanes_for = [&](int64_t plan_bytes) {
+        int64_t l = (budget - plan_bytes) / per_lane;
+        l = std::min<int64_t>(l, 256);
+        return int(l / 32 * 32);
+    };
+    const int la = lanes_for(p.lay.eval_bytes), lb = lanes_for(0);
+    ds->plan_smem = la >= lb;
+    ds->T = ds->plan_smem ? la : lb;
+    if (ds->T >= 32) {
+        ds->lanes = ds->T;
+        ds->smem = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0) +
+                   ((int64_t(ds->T) * ds->ld_cap + 15) & ~int64_t(15)) +
+                   int64_t(p.live_slots) * ds->T * 8 +
+                   (ds->kt == 0 ? int64_t(2) * p.K * ds->T * 8 : 0);
+        int blocks = 0;
+        if (eval_occupancy(ds->kt, cls, ds->T, ds->smem, &blocks) != HS_OK)
+            blocks = 0;
+        ds->blocks_per_sm = blocks;
+    }
+    if (ds->blocks_per_sm < 1) {  // eval unusable; bounds kernels still run
+        ds->T = ds->lanes = 0;
+        ds->smem = 0;
+    }
+    // device blob with slot indices scaled to element offsets in [slot][lane]
+    std::vector<uint8_t> img = p.blob;
+    NodeRec *nodes = reinterpret_cast<NodeRec *>(img.data() + p.lay.node);
+    EdgeRec *edges = reinterpret_cast<EdgeRec *>(img.data() + p.lay.edge);
+    for (int i = 0; i < p.V; ++i)
+        if (nodes[i].out_slot >= 0) nodes[i].out_slot *= ds->lanes;
+    for (size_t q = 0; q < p.edges.size(); ++q) edges[q].slot *= ds->lanes;
+    cudaGetLastError();  // clear a sticky-free error from the occupancy probe
+    e = cudaMalloc(&ds->blob, img.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ds->blob, img.data(), img.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (ds->blob) cudaFree(ds->blob);
+        delete ds;
+        if (err) *err = std::string("plan upload: ") + cudaGetErrorString(e);
+        return HS_ECUDA;
+    }
+    if ((int)p.devs.size() <= dev) p.devs.resize(dev + 1, nullptr);
+    p.devs[dev] = ds;
+    *out = ds;
+    return HS_OK;
+}
+
+}  // namespace hs
+
+namespace {
+
+struct Scratch {
+    void *ptr = nullptr;
+    cudaStream_t s = nullptr;
+    ~Scratch() {
+        if (ptr) cudaFreeAsync(ptr, s);
+    }
+};
+
+// Common body of hs_eval / hs_eval_gen / hs_trace.
+int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
+             int gen, uint64_t seed, int64_t first, const uint8_t *tmpl,
+             const int16_t *group, int n_groups, double *makespan,
+             uint8_t *status, double *starts, uint8_t *genes_out, hs_best *best,
+             int64_t index_base, cudaStream_t stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    const hs::Plan &p = plan->p;
+    if (n < 0) return set_err(HS_EINVAL, "n < 0");
+    if (!gen && n > 0 && p.V > 0 && (!genes || ld < p.V))
+        return set_err(HS_EINVAL, "genes must be [n x ld] with ld >= V");
+    const hs::DevState *ds = nullptr;
+    std::string err;
+    int rc = hs::get_dev_state(p, &ds, &err);
+    if (rc) return set_err(rc, err);
+    if (ds->lanes == 0)
+        return set_err(HS_EINVAL, "graph too large for the shared-memory "
+                                  "evaluator (live end-time slots of one warp "
+                                  "exceed the per-CTA shared memory)");
+
+    Scratch repack;
+    repack.s = stream;
+    if (!gen && n > 0 && ld > ds->ld_cap) {
+        // exotic row stride: compact to the preferred stride first
+        const int64_t pl = p.pref_ld();
+        CK(cudaMallocAsync(&repack.ptr, size_t(n * pl), stream));
+        CK(cudaMemcpy2DAsync(repack.ptr, size_t(pl), genes, size_t(ld),
+                             size_t(p.V), size_t(n), cudaMemcpyDeviceToDevice,
+                             stream));
+        genes = static_cast<const uint8_t *>(repack.ptr);
+        ld = pl;
+    }
+    const int64_t ntiles = (n + ds->lanes - 1) / ds->lanes;
+    const int64_t cap = int64_t(ds->sms) * ds->blocks_per_sm;
+    const int grid = int(std::max<int64_t>(1, std::min(ntiles, cap)));
+
+    Scratch red;
+    red.s = stream;
+    hs::EvalParams a{};
+    if (best) {
+        CK(cudaMallocAsync(&red.ptr, size_t(grid) * sizeof(hs_best) + 16, stream));
+        a.partial = static_cast<hs_best *>(red.ptr);
+        a.ticket = reinterpret_cast<unsigned int *>(
+            static_cast<uint8_t *>(red.ptr) + size_t(grid) * sizeof(hs_best));
+        CK(cudaMemsetAsync(a.ticket, 0, 16, stream));
+    }
+    a.blob = ds->blob;
+    a.lay = p.lay;
+    a.eval_bytes = p.lay.eval_bytes;
+    a.V = p.V;
+    a.K = p.K;
+    a.flags = flags_of(p);
+    a.plan_smem = ds->plan_smem ? 1 : 0;
+    a.lanes = ds->lanes;
+    a.ld_s = gen ? p.pref_ld() : int(ld);
+    a.slots = p.live_slots;
+    a.bulk = (!gen && (reinterpret_cast<uintptr_t>(genes) & 15) == 0) ? 1 : 0;
+    a.genes = genes;
+    a.n = n;
+    a.ld = ld;
+    a.gen = gen;
+    a.seed = seed;
+    a.first = first;
+    a.tmpl = tmpl;
+    a.group = group;
+    a.n_groups = group ? n_groups : p.V;
+    a.makespan = makespan;
+    a.status = status;
+    a.starts = starts;
+    a.genes_out = genes_out;
+    a.best = best;
+    a.index_base = index_base;
+    rc = hs::launch_eval(*ds, !p.uniform_comm, a, grid, stream, &err);
+    if (rc) return set_err(rc, err);
+    return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *hs_last_error(void) { return g_err.c_str(); }
+
+int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+int hs_plan_create(const hs_instance_desc *desc, hs_plan **out) {
+    if (!desc || !out) return set_err(HS_EINVAL, "null argument");
+    hs_plan *pl = new (std::nothrow) hs_plan();
+    if (!pl) return set_err(HS_ENOMEM, "out of host memory");
+    std::string err;
+    int rc = hs::build_plan(*desc, pl->p, &err);
+    if (rc) {
+        delete pl;
+        return set_err(rc, err);
+    }
+    *out = pl;
+    return HS_OK;
+}
+
+void hs_plan_destroy(hs_plan *plan) { delete plan; }
+
+int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info) {
+    if (!plan || !info) return set_err(HS_EINVAL, "null argument");
+    const hs::Plan &p = plan->p;
+    info->V = p.V;
+    info->E = p.E;
+    info->K = p.K;
+    info->L = p.L;
+    info->live_slots = p.live_slots;
+    info->n_classes = p.n_classes;
+    info->uniform_comm = p.uniform_comm;
+    info->full_mesh = p.full_mesh;
+    info->mem_check = p.mem_check;
+    info->all_batch_ok = p.all_batch_ok;
+    info->latency_complete = p.latency_complete;
+    info->words = p.words;
+    info->pref_ld = p.pref_ld();
+    return HS_OK;
+}
+
+int hs_plan_order(const hs_plan *plan, int32_t *order, int32_t *dev_order) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (order) std::copy(plan->p.order.begin(), plan->p.order.end(), order);
+    if (dev_order)
+        std::copy(plan->p.dev_order.begin(), plan->p.dev_order.end(), dev_order);
+    return HS_OK;
+}
+
+int hs_eval(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
+            double *d_makespan, uint8_t *d_status, hs_best *d_best,
+            int64_t index_base, void *stream) {
+    return run_eval(plan, d_genes, n, ld, 0, 0, 0, nullptr, nullptr, 0,
+                    d_makespan, d_status, nullptr, nullptr, d_best, index_base,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int hs_eval_gen_ex(const hs_plan *plan, int mode, uint64_t seed, int64_t first,
+                   int64_t n, const uint8_t *d_template, const int16_t *d_group,
+                   int32_t n_groups, double *d_makespan, uint8_t *d_status,
+                   uint8_t *d_genes_out, hs_best *d_best, void *stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (first < 0) return set_err(HS_EINVAL, "first < 0");
+    if (mode != HS_GEN_RANDOM && mode != HS_GEN_ENUM)
+        return set_err(HS_EINVAL, "unknown generation mode");
+    if (d_group && (n_groups < 0 || n_groups > plan->p.V || !d_template))
+        return set_err(HS_EINVAL, "group map needs a template and "
+                                  "0 <= n_groups <= V");
+    if (mode == HS_GEN_ENUM) {
+        // every enumerated index must be < K^n_groups
+        const int ng = d_group ? n_groups : plan->p.V;
+        long double space = 1.0L;
+        for (int j = 0; j < ng && space < 1e19L; ++j) space *= plan->p.K;
+        if ((long double)first + (long double)n > space)
+            return set_err(HS_EINVAL, "enumeration range exceeds K^groups");
+    }
+    return run_eval(plan, nullptr, n, 0, mode, seed, first, d_template, d_group,
+                    n_groups, d_makespan, d_status, nullptr, d_genes_out, d_best,
+                    first, static_cast<cudaStream_t>(stream));
+}
+
+int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,
+                double *d_makespan, uint8_t *d_status, uint8_t *d_genes_out,
+                hs_best *d_best, void *stream) {
+    return hs_eval_gen_ex(plan, HS_GEN_RANDOM, seed, first, n, nullptr, nullptr,
+                          0, d_makespan, d_status, d_genes_out, d_best, stream);
+}
+
+int hs_trace(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
+             double *d_start, double *d_makespan, uint8_t *d_status,
+             void *stream) {
+    return run_eval(plan, d_genes, n, ld, 0, 0, 0, nullptr, nullptr, 0,
+                    d_makespan, d_status, d_start, nullptr, nullptr, 0,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
+                 int64_t ld, double *h_makespan, uint8_t *h_status,
+                 hs_best *h_best, int64_t index_base, void *stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (n < 0 || (n > 0 && (!h_genes || ld < plan->p.V)))
+        return set_err(HS_EINVAL, "genes must be [n x ld] with ld >= V");
+    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 1 << 19));
+    const int64_t nchunks = n > 0 ? (n + chunk - 1) / chunk : 1;
+    const size_t gbytes = size_t(chunk * ld);
+    const size_t per = ((gbytes + 255) & ~size_t(255)) + size_t(chunk) * 8 +
+                       ((size_t(chunk) + 255) & ~size_t(255));
+    cudaStream_t s1 = nullptr;
+    CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    uint8_t *buf = nullptr;
+    hs_best *bests = nullptr;
+    int rc = HS_OK;
+    do {
+        cudaError_t e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev0, 0);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&buf, 2 * per, s0);
+        if (e == cudaSuccess)
+            e = cudaMallocAsync((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
+        if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev0, 0);
+        if (e != cudaSuccess) {
+            rc = cuda_err(e, "hs_eval_host setup");
+            break;
+        }
+        for (int64_t c = 0; c < nchunks && rc == HS_OK; ++c) {
+            cudaStream_t s = (c & 1) ? s1 : s0;
+            uint8_t *b = buf + (c & 1) * per;
+            uint8_t *dg = b;
+            double *dm = reinterpret_cast<double *>(b + ((gbytes + 255) & ~size_t(255)));
+            uint8_t *dsx = reinterpret_cast<uint8_t *>(dm + chunk);
+            const int64_t lo = c * chunk, rows = std::min(chunk, n - lo);
+            if (rows > 0) {
+                e = cudaMemcpyAsync(dg, h_genes + lo * ld, size_t(rows * ld),
+                                    cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) {
+                    rc = cuda_err(e, "H2D genes");
+                    break;
+                }
+            }
+            rc = run_eval(plan, dg, std::max<int64_t>(rows, 0), ld, 0, 0, 0,
+                          nullptr, nullptr, 0, h_makespan ? dm : nullptr, h_status ? dsx : nullptr,
+                          nullptr, nullptr, h_best ? bests + c : nullptr,
+                          index_base + lo, s);
+            if (rc) break;
+            if (h_makespan && rows > 0)
+                e = cudaMemcpyAsync(h_makespan + lo, dm, size_t(rows) * 8,
+                                    cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess && h_status && rows > 0)
+                e = cudaMemcpyAsync(h_status + lo, dsx, size_t(rows),
+                                    cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) rc = cuda_err(e, "D2H results");
+        }
+        if (rc) break;
+        e = cudaEventRecord(ev1, s1);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, ev1, 0);
+        std::vector<hs_best> hb(static_cast<size_t>(nchunks));
+        if (e == cudaSuccess && h_best)
+            e = cudaMemcpyAsync(hb.data(), bests, size_t(nchunks) * sizeof(hs_best),
+                                cudaMemcpyDeviceToHost, s0);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s0);
+        if (e != cudaSuccess) {
+            rc = cuda_err(e, "hs_eval_host sync");
+            break;
+        }
+        if (h_best) hs_best_merge(hb.data(), nchunks, h_best);
+    } while (0);
+    if (buf) cudaFreeAsync(buf, s0);
+    if (bests) cudaFreeAsync(bests, s0);
+    cudaStreamSynchronize(s1);
+    cudaStreamDestroy(s1);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    return rc;
+}
+
+int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,
+                double *d_out, uint8_t *d_status, void *stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (nsub < 0 || (nsub > 0 && (!d_masks || !d_out)))
+        return set_err(HS_EINVAL, "bad mask arguments");
+    if (nsub == 0) return HS_OK;
+    const hs::Plan &p = plan->p;
+    const hs::DevState *ds = nullptr;
+    std::string err;
+    int rc = hs::get_dev_state(p, &ds, &err);
+    if (rc) return set_err(rc, err);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t step = std::max<int64_t>(
+        1, std::min<int64_t>(nsub, (int64_t(1) << 25) / std::max(p.V, 1)));
+    Scratch sc;
+    sc.s = s;
+    CK(cudaMallocAsync(&sc.ptr, size_t(std::max(p.V, 1)) * size_t(step) * 8, s));
+    for (int64_t lo = 0; lo < nsub; lo += step) {
+        const int64_t m = std::min(step, nsub - lo);
+        rc = hs::launch_cp(ds->blob, p.lay, p.V, std::max(p.words, 1),
+                           d_masks + lo * std::max(p.words, 1), m, d_out + lo,
+                           d_status ? d_status + lo : nullptr,
+                           static_cast<double *>(sc.ptr), s, &err);
+        if (rc) return set_err(rc, err);
+    }
+    return HS_OK;
+}
+
+int hs_reach(const hs_plan *plan, uint64_t *d_desc, uint64_t *d_anc,
+             void *stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    const hs::Plan &p = plan->p;
+    if (p.NT == 0) return HS_OK;
+    const hs::DevState *ds = nullptr;
+    std::string err;
+    int rc = hs::get_dev_state(p, &ds, &err);
+    if (rc) return set_err(rc, err);
+    rc = hs::launch_reach(ds->blob, p.lay, p.NT, p.words, d_desc, d_anc,
+                          static_cast<cudaStream_t>(stream), &err);
+    return rc ? set_err(rc, err) : HS_OK;
+}
+
+int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out) {
+    if (!out || (n > 0 && !bests)) return set_err(HS_EINVAL, "null argument");
+    hs_best b{__builtin_huge_val(), -1};
+    for (int64_t k = 0; k < n; ++k) {
+        if (bests[k].index < 0) continue;
+        const double c = bests[k].cost;
+        if (b.index < 0 || c < b.cost || (c == b.cost && bests[k].index < b.index))
+            b = bests[k];
+    }
+    *out = b;
+    return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,557 @@
+"""Genome encoding, the GPU-backed list-scheduling decoder, and the heuristics
+that consume it -- the drop-in for ``hetsched.heuristics``
+(/root/reference/pkg/src/hetsched/heuristics.py).
+
+* ``decode`` / ``fitness`` (heuristics.py:127-148) evaluate on the B200
+  through the C ABI (hs_trace / hs_eval); results are bit-identical to the
+  reference's Python list scheduler.
+* ``fitness_batch`` / ``argmin_batch`` / ``random_search`` are the batched
+  entry points (no reference counterpart: the reference evaluates one genome
+  per call).
+* ``best_device`` / ``met`` (:151-189) compute their mapping on the host and
+  decode on the GPU; ``greedy`` (:192-210) is a host list scheduler (K-way
+  per-step choice, nothing to batch) used as SA's start.
+* ``simulated_annealing`` / ``one_plus_one_ea`` (:259-334) keep the
+  reference's exact trajectory for a given seed while evaluating their
+  candidates in speculative GPU batches (rng.py replays numpy's stream).
+"""
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from . import rng as R
+from .core import (GraphError, Schedule, ScheduledBatch, ScheduleError,
+                   bfs_topological_order)
+from .plan import Plan, get_plan
+
+INF = float("inf")
+
+
+@dataclass(frozen=True)
+class MappingGenome:
+    genes: tuple[int, ...]  # device index per task, BFS topological positions
+    order: tuple[str, ...]  # the task ordering the positions refer to
+
+    def __post_init__(self):
+        if len(self.genes) != len(self.order):
+            raise GraphError("genome length must equal task count")
+
+
+def genome_from_map(g, hw, mapping: dict) -> MappingGenome:
+    """Genes = index into sorted(hw.devices), positions = BFS order
+    (heuristics.py:34-40)."""
+    order = tuple(bfs_topological_order(g))
+    idx = {u: k for k, u in enumerate(sorted(hw.devices))}
+    return MappingGenome(genes=tuple(idx[mapping[t]] for t in order),
+                         order=order)
+
+
+# ---------------------------------------------------------------------------
+# small-batch evaluation context (one per thread): reuses device buffers so
+# single-genome calls cost one H2D, one launch and one D2H
+
+class _Ctx(threading.local):
+    def __init__(self):
+        self.cap = 0
+        self.genes = self.ms = self.st = self.starts = None
+        self.stream = None
+
+
+_ctx = _Ctx()
+
+
+def _device_buffers(n: int, ld: int, V: int, trace: bool):
+    import torch
+    c = _ctx
+    if c.stream is None:
+        c.stream = torch.cuda.Stream()
+    need = n * ld
+    if c.genes is None or c.genes.numel() < need or c.cap < n:
+        cap = max(n, 2 * c.cap, 64)
+        c.cap = cap
+        c.genes = torch.empty(cap * max(ld, 1) + 16, dtype=torch.uint8,
+                              device="cuda")
+        c.ms = torch.empty(cap, dtype=torch.float64, device="cuda")
+        c.st = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        c.starts = None
+    if trace and (c.starts is None or c.starts.numel() < n * max(V, 1)):
+        c.starts = torch.empty(max(n * V, 1), dtype=torch.float64,
+                               device="cuda")
+    return c
+
+
+def _eval_rows(plan: Plan, rows: np.ndarray, trace: bool = False):
+    """Evaluate uint8 rows [n, V] on the GPU -> (makespan, status[, starts])
+    as numpy arrays."""
+    import torch
+    n, V = rows.shape
+    ld = plan.pref_ld if V else 1
+    c = _device_buffers(n, ld, V, trace)
+    host = np.zeros((n, ld), np.uint8)
+    host[:, :V] = rows
+    with torch.cuda.stream(c.stream):
+        g = c.genes[: n * ld].view(n, ld)
+        g.copy_(torch.from_numpy(host), non_blocking=False)
+        ms, st = c.ms[:n], c.st[:n]
+        if trace:
+            sv = c.starts[: n * V].view(n, V) if V else c.starts[:0]
+            plan.trace(g, c.starts, ms, st, stream=c.stream)
+            out = (ms.cpu().numpy(), st.cpu().numpy(),
+                   sv.cpu().numpy().reshape(n, V))
+        else:
+            plan.eval(g, ms, st, None, stream=c.stream)
+            out = (ms.cpu().numpy(), st.cpu().numpy())
+    return out
+
+
+def _check_genes(genes: Sequence[int], K: int) -> None:
+    # heuristics.py:133-134: validated before any placement
+    if any(not 0 <= int(k) < K for k in genes):
+        raise GraphError("gene value out of device range")
+
+
+def _raise_status(st: int) -> None:
+    if st == N.ST_GENE:
+        raise GraphError("gene value out of device range")
+    if st == N.ST_MISSING:
+        raise GraphError("missing latency entry for a reached (task, device, "
+                         "batch) placement")
+
+
+def decode(genome: MappingGenome, g, hw, table, L: int) -> Optional[Schedule]:
+    """List-schedule the genome's mapping in its order at the earliest
+    feasible start (heuristics.py:127-143), on the GPU. Returns None for
+    structurally infeasible genomes."""
+    _check_genes(genome.genes, len(hw.devices))
+    if len(genome.order) == 0:
+        return Schedule(batches=(), objective=0.0, input_count=L)
+    plan = get_plan(g, hw, table, L, genome.order)
+    rows = np.asarray(genome.genes, np.uint8)[None, :]
+    ms, st, starts = _eval_rows(plan, rows, trace=True)
+    s = int(st[0])
+    _raise_status(s)
+    if s != N.ST_OK:
+        return None
+    inputs = tuple(range(1, L + 1))
+    devs = sorted(hw.devices)
+    batches = tuple(
+        ScheduledBatch(task=t, device=devs[genome.genes[i]], size=L,
+                       inputs=inputs, start=float(starts[0, i]))
+        for i, t in enumerate(genome.order))
+    return Schedule(batches=batches, objective=float(ms[0]), input_count=L)
+
+
+def fitness(genome: MappingGenome, g, hw, table, L: int) -> float:
+    """Makespan of the decoded genome, +inf when infeasible
+    (heuristics.py:146-148)."""
+    _check_genes(genome.genes, len(hw.devices))
+    if len(genome.order) == 0:
+        return 0.0
+    plan = get_plan(g, hw, table, L, genome.order)
+    ms, st = _eval_rows(plan, np.asarray(genome.genes, np.uint8)[None, :])
+    _raise_status(int(st[0]))
+    return float(ms[0])
+
+
+# ---------------------------------------------------------------------------
+# batched API
+
+def fitness_batch(genes, g, hw, table, L: int, *,
+                  order: Optional[Sequence[str]] = None,
+                  return_status: bool = False, index_base: int = 0):
+    """Makespans of many genomes in one launch.
+
+    ``genes`` is a uint8 [n, >=V] array of sorted-device indices in genome
+    order (BFS unless ``order``): a numpy array (host path, hs_eval_host)
+    or a CUDA torch tensor (device path, hs_eval; results stay on device).
+    Raises GraphError where the reference's ``fitness`` would (gene out of
+    range, missing latency entry) unless ``return_status`` is set, in which
+    case (makespan, status) is returned.
+    """
+    plan = get_plan(g, hw, table, L, order)
+    if hasattr(genes, "data_ptr"):  # torch tensor on the GPU
+        import torch
+        if genes.dtype != torch.uint8 or genes.dim() != 2 \
+                or genes.shape[1] < plan.V or (genes.numel() and
+                                               genes.stride(1) != 1):
+            raise GraphError("genes must be a uint8 [n, >=V] row-major tensor")
+        n = genes.shape[0]
+        ms = torch.empty(n, dtype=torch.float64, device=genes.device)
+        st = torch.empty(n, dtype=torch.uint8, device=genes.device)
+        plan.eval(genes, ms, st, None, index_base)
+        if return_status:
+            return ms, st
+        worst = int(st.max().item()) if n else 0
+        if worst >= N.ST_MISSING:
+            bad = int(torch.nonzero(st >= N.ST_MISSING)[0].item())
+            _raise_status(int(st[bad].item()))
+        return ms
+    genes = np.asarray(genes)
+    if genes.ndim != 2 or genes.shape[1] < plan.V:
+        raise GraphError("genes must be a [n, >=V] array")
+    if genes.dtype != np.uint8:
+        out_of_range = (genes < 0) | (genes >= plan.K)
+        if out_of_range.any() and not return_status:
+            raise GraphError("gene value out of device range")
+        # anything outside [0, 255] becomes 255 (still out of range: status 5)
+        genes = np.where((genes < 0) | (genes > 255), 255,
+                         genes).astype(np.uint8)
+    n = genes.shape[0]
+    ms = np.empty(n, np.float64)
+    st = np.empty(n, np.uint8)
+    plan.eval_host(genes, ms, st, None, index_base)
+    if return_status:
+        return ms, st
+    if n and st.max() >= N.ST_MISSING:
+        _raise_status(int(st[np.argmax(st >= N.ST_MISSING)]))
+    return ms
+
+
+def throughput(makespan, L: int):
+    """Inputs per second, 1000 * L / makespan (cli.py:154, bounds.py:234);
+    +inf where the makespan is 0 (the reference prints no throughput)."""
+    m = np.asarray(makespan, np.float64)
+    with np.errstate(divide="ignore"):
+        out = (1000.0 * L) / m
+    return np.where(m > 0, out, INF)
+
+
+def argmin_batch(genes, g, hw, table, L: int, *,
+                 order: Optional[Sequence[str]] = None,
+                 index_base: int = 0) -> tuple[float, int]:
+    """(makespan, index) of the first best genome (numpy.argmin semantics,
+    +inf allowed) computed by the fused on-device reduction."""
+    plan = get_plan(g, hw, table, L, order)
+    if hasattr(genes, "data_ptr"):
+        import torch
+        best = torch.empty(2, dtype=torch.int64, device=genes.device)
+        plan.eval(genes, None, None, best, index_base)
+        b = best.cpu()
+        return float(b[:1].view(torch.float64).item()), int(b[1].item())
+    genes = np.ascontiguousarray(genes, np.uint8)
+    b = N.Best()
+    plan.eval_host(genes, None, None, b, index_base)
+    return float(b.cost), int(b.index)
+
+
+def random_search(g, hw, table, L: int, n: int, *, seed: int = 0,
+                  first: int = 0, chunk: int = 1 << 26):
+    """Evaluate n on-device generated genomes (oracle gen_genes(seed, c) for
+    c in [first, first + n)) and return (best makespan, index, genome)."""
+    import torch
+    plan = get_plan(g, hw, table, L)
+    bests = []
+    dbest = torch.empty(2, dtype=torch.int64, device="cuda")
+    for lo in range(first, first + n, chunk):
+        m = min(chunk, first + n - lo)
+        plan.eval_gen(N.GEN_RANDOM, seed, lo, m, best=dbest)
+        b = dbest.cpu()
+        bests.append((float(b[:1].view(torch.float64).item()),
+                      int(b[1].item())))
+    cost, idx = min(bests, key=lambda t: (t[0], t[1])) if bests \
+        else (INF, -1)
+    genome = None
+    if idx >= 0:
+        out = torch.empty((1, plan.V), dtype=torch.uint8, device="cuda")
+        plan.eval_gen(N.GEN_RANDOM, seed, idx, 1, genes_out=out)
+        genome = MappingGenome(genes=tuple(int(x) for x in out.cpu()[0]),
+                               order=plan.order)
+    return cost, idx, genome
+
+
+# ---------------------------------------------------------------------------
+# baseline heuristics
+
+def best_device(g, hw, table, L: int) -> Schedule:
+    """Whole graph serially on the single fastest device
+    (heuristics.py:151-167)."""
+    best = None
+    for u in sorted(hw.devices):
+        if L not in hw.devices[u].batch_sizes:
+            continue
+        total = sum(table.get(i, u, L) for i in g.tasks)
+        if best is None or total < best[0] - 1e-12:
+            best = (total, u)
+    if best is None:
+        raise ScheduleError(f"no device supports batch size {L}")
+    s = decode(genome_from_map(g, hw, {i: best[1] for i in g.tasks}),
+               g, hw, table, L)
+    if s is None:
+        raise ScheduleError(f"device {best[1]!r} cannot hold the whole graph")
+    return s
+
+
+def _met_mapping(g, hw, table, L: int) -> dict:
+    mapping = {}
+    devs = sorted(hw.devices)
+    for i in g.tasks:
+        best = None
+        for u in devs:
+            if L not in hw.devices[u].batch_sizes:
+                continue
+            ms = table.get(i, u, L)
+            if best is None or ms < best[0] - 1e-12:
+                best = (ms, u)
+        if best is None:
+            raise ScheduleError(f"no device supports batch size {L}")
+        mapping[i] = best[1]
+    return mapping
+
+
+def met(g, hw, table, L: int) -> Schedule:
+    """Each task on its minimum-execution-time device, ties to the smallest
+    device id (heuristics.py:170-189)."""
+    s = decode(genome_from_map(g, hw, _met_mapping(g, hw, table, L)),
+               g, hw, table, L)
+    if s is None:
+        raise ScheduleError("MET mapping infeasible (missing links or memory)")
+    return s
+
+
+class _HostScheduler:
+    """Host restatement of the non-insertion list scheduler for the K-way
+    greedy choice (heuristics.py:43-124); per-step work is O(K * preds)."""
+
+    def __init__(self, g, hw, table, L: int):
+        self.g, self.hw, self.table, self.L = g, hw, table, L
+        self.avail = {u: 0.0 for u in hw.devices}
+        self.mem = {u: 0.0 for u in hw.devices}
+        self.end: dict[str, tuple[str, float]] = {}
+        self.batches: list[ScheduledBatch] = []
+        self.makespan = 0.0
+
+    def try_place(self, task: str, dev: str):
+        node = self.g.tasks[task]
+        d = self.hw.devices[dev]
+        if self.L not in d.batch_sizes:
+            return None
+        extra = (node.im + node.om) * self.L
+        extra += node.wm
+        if self.mem[dev] + extra > d.memory + 1e-9:
+            return None
+        ready = 0.0
+        for p in self.g.pred[task]:
+            src, e = self.end[p]
+            c = self.hw.comm_time(self.g.tasks[p].om, src, dev)
+            if c is None:
+                return None
+            x = e + c
+            if x > ready:
+                ready = x
+        dur = self.table.get(task, dev, self.L)
+        a = self.avail[dev]
+        start = a if a > ready else ready
+        return start, start + dur, extra
+
+    def commit(self, task, dev, start, end, extra):
+        self.avail[dev] = end
+        self.mem[dev] += extra
+        self.end[task] = (dev, end)
+        self.batches.append(ScheduledBatch(
+            task=task, device=dev, size=self.L,
+            inputs=tuple(range(1, self.L + 1)), start=start))
+        if end > self.makespan:
+            self.makespan = end
+
+
+def greedy(g, hw, table, L: int) -> Schedule:
+    """BFS order, each task where the partial makespan grows least
+    (heuristics.py:192-210)."""
+    ls = _HostScheduler(g, hw, table, L)
+    devs = sorted(hw.devices)
+    for task in bfs_topological_order(g):
+        choice = None
+        for u in devs:
+            spot = ls.try_place(task, u)
+            if spot is None:
+                continue
+            cand = spot[1] if spot[1] > ls.makespan else ls.makespan
+            if choice is None or cand < choice[0] - 1e-12:
+                choice = (cand, u, spot)
+        if choice is None:
+            raise ScheduleError(f"no feasible placement for task {task!r}")
+        ls.commit(task, choice[1], *choice[2])
+    return Schedule(batches=tuple(ls.batches), objective=ls.makespan,
+                    input_count=L)
+
+
+# ---------------------------------------------------------------------------
+# search loops with exact speculative GPU batches
+
+def _fit_rows(plan: Plan, rows: np.ndarray) -> np.ndarray:
+    ms, st = _eval_rows(plan, rows)
+    if st.size and st.max() >= N.ST_MISSING:
+        _raise_status(int(st[np.argmax(st >= N.ST_MISSING)]))
+    return ms
+
+
+def simulated_annealing(g, hw, table, L: int, seed: int = 0,
+                        budget: int = 2000, t0_fraction: float = 0.1,
+                        alpha: float = 0.995, window: int = 64) -> Schedule:
+    """Single-gene reassignment, geometric cooling, Metropolis acceptance,
+    greedy start, best-ever genome decoded (heuristics.py:259-299).
+
+    Same trajectory as the reference for the same seed. Each GPU batch holds
+    the candidates of the next `window` steps for every stream position the
+    run can reach if those steps are rejected (a step draws ``random()`` only
+    when the candidate is finite and worse, so positions branch); the host
+    replays the steps against the batch until the first acceptance.
+    """
+    gen = np.random.default_rng(seed)
+    start = greedy(g, hw, table, L)
+    mapping = {b.task: b.device for b in start.batches}
+    cur = genome_from_map(g, hw, mapping)
+    cur_fit = fitness(cur, g, hw, table, L)
+    best, best_fit = cur, cur_fit
+    temp = max(t0_fraction * cur_fit, 1e-9)
+    n_dev = len(hw.devices)
+    V = len(cur.genes)
+    plan = get_plan(g, hw, table, L)
+    genes = np.array(cur.genes, np.uint8)
+    step = 0
+    k = max(1, min(window, 8))
+    while step < budget:
+        k = min(k, budget - step)
+        S, st0 = R.peek(gen, 4 * k + 64)
+
+        def draw(st):
+            pos, st = S.integers(st, V)
+            old = int(genes[pos])
+            if n_dev > 1:
+                new, st = S.integers(st, n_dev - 1)
+                if new >= old:
+                    new += 1
+            else:
+                new = old
+            return pos, new, st
+
+        # candidates for every state reachable through rejected steps
+        cand: dict[tuple, tuple] = {}
+        frontier = {st0}
+        try:
+            for _ in range(k):
+                nxt = set()
+                for s in frontier:
+                    if s not in cand:
+                        pos, new, s2 = draw(s)
+                        cand[s] = (pos, new, s2)
+                    s2 = cand[s][2]
+                    nxt.add(s2)
+                    nxt.add(S.next64(s2)[1])
+                frontier = nxt
+        except IndexError:  # ran out of peeked words: shorter window
+            pass
+        keys = list(cand)
+        rows = np.repeat(genes[None, :], len(keys), axis=0)
+        for r, s in enumerate(keys):
+            pos, new, _ = cand[s]
+            rows[r, pos] = new
+        fits = _fit_rows(plan, rows)
+        fit_of = {s: float(fits[r]) for r, s in enumerate(keys)}
+        # replay the reference's steps
+        s = st0
+        accepted = False
+        for _ in range(k):
+            if s not in cand:
+                break
+            pos, new, s2 = cand[s]
+            cand_fit = fit_of[s]
+            delta = cand_fit - cur_fit
+            accept = delta <= 0
+            s = s2
+            if not accept and math.isfinite(cand_fit):
+                u, s = S.random(s)
+                accept = u < math.exp(-delta / temp)
+            step += 1
+            if accept:
+                genes = genes.copy()
+                genes[pos] = new
+                cur_fit = cand_fit
+                if cand_fit < best_fit:
+                    best, best_fit = genes.copy(), cand_fit
+                accepted = True
+            temp *= alpha
+            if accepted:
+                break
+        R.commit(gen, s)
+        k = 8 if accepted else min(window, 2 * k)
+    best_genes = best.genes if isinstance(best, MappingGenome) \
+        else tuple(int(x) for x in best)
+    out = decode(MappingGenome(genes=tuple(best_genes), order=cur.order),
+                 g, hw, table, L)
+    assert out is not None
+    return out
+
+
+def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
+                    biased: bool = True, window: int = 256) -> Schedule:
+    """(1+1) EA: each gene mutated with probability 1/|V|, accept when not
+    worse; biased start = MET, unbiased = uniform genes
+    (heuristics.py:302-334). The mutation stream does not depend on fitness,
+    so `window` children are drawn ahead and evaluated in one GPU batch;
+    an acceptance re-bases the remaining children (same trajectory as the
+    reference)."""
+    gen = np.random.default_rng(seed)
+    order = tuple(bfs_topological_order(g))
+    n_dev = len(hw.devices)
+    V = len(order)
+    if biased:
+        cur = genome_from_map(g, hw, {b.task: b.device for b in
+                                      met(g, hw, table, L).batches})
+    else:
+        cur = MappingGenome(
+            genes=tuple(int(v) for v in gen.integers(n_dev, size=V)),
+            order=order)
+    cur_fit = fitness(cur, g, hw, table, L)
+    p = 1.0 / max(V, 1)
+    genes = np.array(cur.genes, np.uint8)
+    plan = get_plan(g, hw, table, L) if V else None
+    step = 0
+    while step < budget:
+        k = min(window, budget - step)
+        S, st = R.peek(gen, k * (V + 2) + 64)
+        muts = []
+        try:
+            for _ in range(k):
+                m = []
+                for pos in range(V):
+                    u, st = S.random(st)
+                    if u < p:
+                        val, st = S.integers(st, n_dev)
+                        m.append((pos, val))
+                muts.append((m, st))
+        except IndexError:
+            pass
+        if not muts:
+            raise RuntimeError("RNG peek window too small")
+        j = 0
+        while j < len(muts):
+            rows = np.repeat(genes[None, :], len(muts) - j, axis=0)
+            for r in range(j, len(muts)):
+                for pos, val in muts[r][0]:
+                    rows[r - j, pos] = val
+            fits = _fit_rows(plan, rows) if V else np.zeros(len(rows))
+            acc = None
+            for r in range(len(rows)):
+                if fits[r] <= cur_fit:
+                    acc = r
+                    break
+            if acc is None:
+                j = len(muts)
+                break
+            genes = rows[acc].copy()
+            cur_fit = float(fits[acc])
+            j += acc + 1
+        step += len(muts)
+        R.commit(gen, muts[-1][1])
+    final = decode(MappingGenome(genes=tuple(int(x) for x in genes),
+                                 order=order), g, hw, table, L)
+    if final is None:
+        raise ScheduleError("EA produced an infeasible genome")
+    return final

@@ -1,0 +1,252 @@
+"""Evaluation plans: (graph, hardware, latency table, L[, genome order]) ->
+native ``hs_plan`` handle, plus the device-side entry points that use it.
+
+A plan is compiled once per instance by the native plan compiler
+(csrc/plan.cpp) and cached on object identity: the reference's graph,
+hardware and latency objects are immutable after construction
+(core.py:38 of the reference), so identity is a sound key.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from collections import OrderedDict
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .core import GraphError
+
+
+def _i64(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _i32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _f64(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _u8(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def _strings(ids):
+    raw = [s.encode("utf-8", "surrogatepass") for s in ids]
+    off = np.zeros(len(raw) + 1, np.int64)
+    off[1:] = np.cumsum([len(b) for b in raw])
+    return b"".join(raw), off
+
+
+class Plan:
+    """Native evaluation plan of one instance at load L."""
+
+    def __init__(self, g, hw, table, L: int,
+                 order: Optional[Sequence[str]] = None):
+        lib = N.load()
+        task_ids = list(g.tasks)
+        tix = {t: k for k, t in enumerate(task_ids)}
+        dev_ids = list(hw.devices)
+        K = len(dev_ids)
+        tnodes = [g.tasks[t] for t in task_ids]
+        wm = np.array([float(t.wm) for t in tnodes], np.float64)
+        im = np.array([float(t.im) for t in tnodes], np.float64)
+        om = np.array([float(t.om) for t in tnodes], np.float64)
+        src = np.array([tix[a] for a, _ in g.edges], np.int32)
+        dst = np.array([tix[b] for _, b in g.edges], np.int32)
+        devs = [hw.devices[u] for u in dev_ids]
+        memory = np.array([float(d.memory) for d in devs], np.float64)
+        sizes = [tuple(int(b) for b in d.batch_sizes) for d in devs]
+        boff = np.zeros(K + 1, np.int32)
+        boff[1:] = np.cumsum([len(s) for s in sizes])
+        bs = np.array([b for s in sizes for b in s], np.int32)
+        bw = np.zeros((K, K), np.float64)
+        for (a, b), v in hw.bandwidth.items():
+            bw[dev_ids.index(a), dev_ids.index(b)] = float(v)
+        cols = [(u, b) for u, s in zip(dev_ids, sizes) for b in s]
+        ent = table.entries
+        lat = np.zeros((len(task_ids), max(len(cols), 1)), np.float64)
+        ok = np.zeros(lat.shape, np.uint8)
+        for r, t in enumerate(task_ids):
+            for c, (u, b) in enumerate(cols):
+                v = ent.get((t, u, b))
+                if v is not None:
+                    lat[r, c] = v
+                    ok[r, c] = 1
+        tid_bytes, toff = _strings(task_ids)
+        did_bytes, doff = _strings(dev_ids)
+        order_arr = None
+        if order is not None:
+            try:
+                order_arr = np.array([tix[t] for t in order], np.int32)
+            except KeyError as exc:
+                raise GraphError(f"genome order names unknown task {exc}")
+            if len(order_arr) != len(task_ids):
+                raise GraphError("genome length must equal task count")
+        # keep every buffer alive for the duration of the call
+        self._keep = (wm, im, om, src, dst, memory, boff, bs, bw, lat, ok,
+                      tid_bytes, toff, did_bytes, doff, order_arr)
+        d = N.InstanceDesc(
+            n_tasks=len(task_ids), task_ids=tid_bytes, task_id_off=_i64(toff),
+            wm=_f64(wm), im=_f64(im), om=_f64(om),
+            n_edges=len(src), edge_src=_i32(src), edge_dst=_i32(dst),
+            n_devices=K, dev_ids=did_bytes, dev_id_off=_i64(doff),
+            memory=_f64(memory), batch_off=_i32(boff), batch_sizes=_i32(bs),
+            bandwidth=_f64(bw), L=int(L), latency=_f64(lat),
+            latency_ok=_u8(ok),
+            order=_i32(order_arr) if order_arr is not None else None)
+        if K == 0:
+            raise GraphError("gene value out of device range")
+        h = C.c_void_p()
+        N.check(lib.hs_plan_create(C.byref(d), C.byref(h)), "plan")
+        self._keep = None
+        self.handle = h
+        self._lib = lib
+        info = N.PlanInfo()
+        N.check(lib.hs_plan_get_info(h, C.byref(info)))
+        self.info = info
+        self.V, self.K, self.L = info.V, info.K, int(L)
+        o = np.zeros(max(self.V, 1), np.int32)
+        dv = np.zeros(K, np.int32)
+        N.check(lib.hs_plan_order(h, o.ctypes.data, dv.ctypes.data))
+        self.task_ids = task_ids
+        self.order = tuple(task_ids[k] for k in o[:self.V])
+        self.devices = tuple(dev_ids[k] for k in dv)  # gene k -> device id
+        self.pref_ld = info.pref_ld
+        self.words = info.words
+        self._reach = None
+        self._lock = threading.Lock()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.hs_plan_destroy(h)
+            except Exception:
+                pass
+
+    # ---------------------------------------------------------- device calls
+    @staticmethod
+    def _stream(stream=None) -> int:
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return int(stream.cuda_stream)
+
+    def eval(self, genes, makespan=None, status=None, best=None,
+             index_base: int = 0, stream=None) -> None:
+        """hs_eval on device tensors: genes uint8 [n, ld] (ld >= V)."""
+        n = int(genes.shape[0])
+        ld = max(int(genes.stride(0)), self.V) if genes.numel() else self.V
+        N.check(self._lib.hs_eval(
+            self.handle, genes.data_ptr() if genes.numel() else None, n, ld,
+            _ptr(makespan), _ptr(status), _ptr(best), int(index_base),
+            self._stream(stream)), "hs_eval")
+
+    def eval_host(self, genes: np.ndarray, makespan=None, status=None,
+                  best: Optional[N.Best] = None, index_base: int = 0,
+                  stream=None) -> None:
+        """hs_eval_host: numpy uint8 [n, ld] host genes, results to host."""
+        genes = np.ascontiguousarray(genes, dtype=np.uint8) \
+            if genes.strides[-1] != 1 else genes
+        n = genes.shape[0]
+        ld = genes.strides[0] if n else self.V
+        N.check(self._lib.hs_eval_host(
+            self.handle, genes.ctypes.data if n else None, n, ld,
+            makespan.ctypes.data if makespan is not None else None,
+            status.ctypes.data if status is not None else None,
+            C.byref(best) if best is not None else None, int(index_base),
+            self._stream(stream)), "hs_eval_host")
+
+    def eval_gen(self, mode: int, seed: int, first: int, n: int,
+                 template=None, group=None, n_groups: int = 0,
+                 makespan=None, status=None, genes_out=None, best=None,
+                 stream=None) -> None:
+        N.check(self._lib.hs_eval_gen_ex(
+            self.handle, int(mode), int(seed) & 0xFFFFFFFFFFFFFFFF,
+            int(first), int(n), _ptr(template), _ptr(group), int(n_groups),
+            _ptr(makespan), _ptr(status), _ptr(genes_out), _ptr(best),
+            self._stream(stream)), "hs_eval_gen")
+
+    def trace(self, genes, starts, makespan, status, stream=None) -> None:
+        n, ld = int(genes.shape[0]), int(genes.stride(0))
+        N.check(self._lib.hs_trace(
+            self.handle, genes.data_ptr(), n, ld, starts.data_ptr(),
+            makespan.data_ptr(), status.data_ptr(), self._stream(stream)),
+            "hs_trace")
+
+    def cp_bound(self, masks, out, status, stream=None) -> None:
+        N.check(self._lib.hs_cp_bound(
+            self.handle, masks.data_ptr(), int(masks.shape[0]),
+            out.data_ptr(), status.data_ptr(), self._stream(stream)),
+            "hs_cp_bound")
+
+    def reach(self):
+        """(desc, anc) uint64 bitsets [n_tasks, words] as numpy (cached)."""
+        with self._lock:
+            if self._reach is None:
+                import torch
+                nt, w = len(self.task_ids), max(self.words, 1)
+                desc = torch.zeros((nt, w), dtype=torch.int64, device="cuda")
+                anc = torch.zeros((nt, w), dtype=torch.int64, device="cuda")
+                N.check(self._lib.hs_reach(self.handle, desc.data_ptr(),
+                                           anc.data_ptr(), self._stream()),
+                        "hs_reach")
+                self._reach = (desc.cpu().numpy().view(np.uint64),
+                               anc.cpu().numpy().view(np.uint64))
+            return self._reach
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return C.addressof(t)
+
+
+# ---------------------------------------------------------------------------
+# identity cache
+
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_LOCK = threading.Lock()
+_CACHE_MAX = 64
+
+
+def _ref(o):
+    try:
+        return weakref.ref(o)
+    except TypeError:
+        return lambda o=o: o  # not weak-referenceable: hold it
+
+
+def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None
+             ) -> Plan:
+    """Cached plan for (g, hw, table, L, order); `order` None or equal to
+    the graph's BFS order selects the default plan."""
+    if order is not None:
+        order = tuple(order)
+        if order == tuple(g._topo):
+            order = None
+    key = (id(g), id(hw), id(table), int(L), order)
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None:
+            refs, plan = hit
+            if refs[0]() is g and refs[1]() is hw and refs[2]() is table:
+                _CACHE.move_to_end(key)
+                return plan
+            del _CACHE[key]
+    plan = Plan(g, hw, table, L, order)
+    with _CACHE_LOCK:
+        _CACHE[key] = ((_ref(g), _ref(hw), _ref(table)), plan)
+        while len(_CACHE) > _CACHE_MAX:
+            _CACHE.popitem(last=False)
+    return plan

@@ -1,0 +1,70 @@
+"""Heuristic drivers on the GPU evaluator against the reference's recorded
+results (tests/golden/heuristics.json): best-device, MET, greedy, and the
+exact SA / (1+1) EA trajectories at fixed seeds."""
+from __future__ import annotations
+
+import pytest
+
+from conftest import fhex, golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2308_00127_b200 as hs  # noqa: E402
+
+
+def _entries():
+    return golden("heuristics")
+
+
+def _cmp(res, s):
+    if "error" in res:
+        return False
+    return fhex(s.objective) == res["objective"] and \
+        {b.task: b.device for b in s.batches} == res["mapping"]
+
+
+@pytest.mark.parametrize("idx", range(14))
+def test_baselines(idx):
+    e = _entries()[idx]
+    g, hw, t = hs.load_instance(e)
+    L = e["L"]
+    for fn, label in ((hs.best_device, "best_device"), (hs.met, "met"),
+                      (hs.greedy, "greedy")):
+        res = e[label]
+        if "error" in res:
+            with pytest.raises(hs.ScheduleError):
+                fn(g, hw, t, L)
+        else:
+            assert _cmp(res, fn(g, hw, t, L)), (label, e["name"])
+
+
+@pytest.mark.parametrize("idx", range(14))
+def test_search_trajectories(idx):
+    e = _entries()[idx]
+    g, hw, t = hs.load_instance(e)
+    L = e["L"]
+    for run in e["search"]:
+        kw = dict(seed=run["seed"], budget=run["budget"])
+        if run["algo"] == "sa":
+            call = lambda: hs.simulated_annealing(g, hw, t, L, **kw)  # noqa
+        else:
+            call = lambda: hs.one_plus_one_ea(  # noqa
+                g, hw, t, L, biased=(run["algo"] == "ea"), **kw)
+        if "error" in run:
+            with pytest.raises(hs.ScheduleError):
+                call()
+        else:
+            assert _cmp(run, call()), (e["name"], run["algo"], run["seed"],
+                                       run["budget"])
+
+
+def test_sa_window_sizes_agree():
+    e = [x for x in _entries() if x["name"] == "ws30"][0]
+    g, hw, t = hs.load_instance(e)
+    a = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=1)
+    b = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=128)
+    assert a == b
+    c = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=1)
+    d = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=97)
+    assert c == d
