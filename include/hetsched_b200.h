@@ -110,6 +110,16 @@ int hs_abi_version(void);
 int hs_plan_create(const hs_instance_desc *desc, hs_plan **out);
 void hs_plan_destroy(hs_plan *plan);
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
+/* Specialise the evaluator to this plan on the current device: the plan is
+ * emitted as straight-line CUDA and compiled by NVRTC for sm_100a (one-time
+ * cost, reported in *compile_ms); later hs_eval* calls on this device use
+ * it. HS_EINVAL when the plan is outside the specialised scope (K <= 4,
+ * one bandwidth over a full mesh, no capacity / batch-size / missing-entry
+ * / NaN cases); the ahead-of-time kernel then keeps serving the plan. */
+int hs_plan_specialize(const hs_plan *plan, double *compile_ms);
+/* The CUDA source the specialiser would compile for `lanes` lanes. */
+int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
+                             int64_t cap, int64_t *len);
 /* genome order (task index per position) and sorted device order */
 int hs_plan_order(const hs_plan *plan, int32_t *order, int32_t *dev_order);
 

@@ -17,7 +17,7 @@ from .core import (Device, DnnGraph, GraphError, HardwareSystem,
 from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
                          fitness, fitness_batch, genome_from_map, greedy, met,
                          one_plus_one_ea, random_search, simulated_annealing,
-                         throughput)
+                         specialize, throughput)
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
                      dep_subgraph, lower_bound, pre_subgraph)
 from .splitting import ModuleSolver, gpu_module_solver

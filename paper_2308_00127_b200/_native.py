@@ -82,6 +82,9 @@ def load() -> C.CDLL:
             "hs_plan_destroy": (None, [vp]),
             "hs_plan_get_info": (C.c_int, [vp, _p(PlanInfo)]),
             "hs_plan_order": (C.c_int, [vp, vp, vp]),
+            "hs_plan_specialize": (C.c_int, [vp, _p(C.c_double)]),
+            "hs_plan_emit_specialized": (C.c_int, [vp, i32, vp, i64,
+                                                   _p(C.c_int64)]),
             "hs_eval": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
             "hs_eval_host": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
             "hs_eval_gen": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp,
@@ -106,7 +109,8 @@ def load() -> C.CDLL:
 def exported_symbols() -> list[str]:
     """Names declared by include/hetsched_b200.h (checked by the tests)."""
     return ["hs_last_error", "hs_abi_version", "hs_plan_create",
-            "hs_plan_destroy", "hs_plan_get_info", "hs_plan_order", "hs_eval",
+            "hs_plan_destroy", "hs_plan_get_info", "hs_plan_order",
+            "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
             "hs_cp_bound", "hs_reach", "hs_best_merge"]
 

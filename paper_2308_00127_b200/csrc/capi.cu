@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "jit.hpp"
 #include "kernels.cuh"
 #include "plan.hpp"
 
@@ -62,7 +63,24 @@ Plan::~Plan() {
         }
         delete d;
     }
+    for (JitModule *m : jits) {
+        if (!m) continue;
+        cudaSetDevice(m->device);
+        jit_free(m);
+    }
     if (cur >= 0) cudaSetDevice(cur);
+}
+
+static bool jit_enabled() {
+    const char *v = getenv("HS_JIT");
+    return !(v && v[0] == '0');
+}
+
+// specialised module for the current device, or null
+const JitModule *find_jit(const Plan &p, int dev) {
+    if (!jit_enabled()) return nullptr;
+    std::lock_guard<std::mutex> lk(p.mu);
+    return (int)p.jits.size() > dev ? p.jits[dev] : nullptr;
 }
 
 int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
@@ -95,13 +113,16 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
         return int(l / 32 * 32);
     };
     const int la = lanes_for(p.lay.eval_bytes), lb = lanes_for(0);
-    ds->plan_smem = la >= lb;
+    // plan tables in shared memory unless that costs more than one warp
+    ds->plan_smem = la >= 32 && la >= lb - 32;
     ds->T = ds->plan_smem ? la : lb;
     if (ds->T >= 32) {
         ds->lanes = ds->T;
-        ds->smem = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0) +
-                   ((int64_t(ds->T) * ds->ld_cap + 15) & ~int64_t(15)) +
-                   int64_t(p.live_slots) * ds->T * 8 +
+        ds->smem_tile = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0);
+        ds->smem_ends = ds->smem_tile +
+                        ((int64_t(ds->T) * ds->ld_cap + 15) & ~int64_t(15));
+        ds->smem_kstate = ds->smem_ends + int64_t(p.live_slots) * ds->T * 8;
+        ds->smem = ds->smem_kstate +
                    (ds->kt == 0 ? int64_t(2) * p.K * ds->T * 8 : 0);
         int blocks = 0;
         if (eval_occupancy(ds->kt, cls, ds->T, ds->smem, &blocks) != HS_OK)
@@ -179,8 +200,11 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
         genes = static_cast<const uint8_t *>(repack.ptr);
         ld = pl;
     }
-    const int64_t ntiles = (n + ds->lanes - 1) / ds->lanes;
-    const int64_t cap = int64_t(ds->sms) * ds->blocks_per_sm;
+    const hs::JitModule *jm = hs::find_jit(p, ds->device);
+    const int lanes = jm ? jm->lanes : ds->lanes;
+    const int64_t ntiles = (n + lanes - 1) / lanes;
+    const int64_t cap = jm ? int64_t(jm->sms) * jm->blocks_per_sm
+                           : int64_t(ds->sms) * ds->blocks_per_sm;
     const int grid = int(std::max<int64_t>(1, std::min(ntiles, cap)));
 
     Scratch red;
@@ -188,7 +212,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     hs::EvalParams a{};
     if (best) {
         CK(cudaMallocAsync(&red.ptr, size_t(grid) * sizeof(hs_best) + 16, stream));
-        a.partial = static_cast<hs_best *>(red.ptr);
+        a.partial = static_cast<hsk::Best *>(red.ptr);
         a.ticket = reinterpret_cast<unsigned int *>(
             static_cast<uint8_t *>(red.ptr) + size_t(grid) * sizeof(hs_best));
         CK(cudaMemsetAsync(a.ticket, 0, 16, stream));
@@ -200,7 +224,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.K = p.K;
     a.flags = flags_of(p);
     a.plan_smem = ds->plan_smem ? 1 : 0;
-    a.lanes = ds->lanes;
+    a.lanes = lanes;
     a.ld_s = gen ? p.pref_ld() : int(ld);
     a.slots = p.live_slots;
     a.bulk = (!gen && (reinterpret_cast<uintptr_t>(genes) & 15) == 0) ? 1 : 0;
@@ -217,9 +241,17 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.status = status;
     a.starts = starts;
     a.genes_out = genes_out;
-    a.best = best;
+    a.best = reinterpret_cast<hsk::Best *>(best);
     a.index_base = index_base;
-    rc = hs::launch_eval(*ds, !p.uniform_comm, a, grid, stream, &err);
+    a.smem_tile = jm ? jm->smem_tile : ds->smem_tile;
+    a.smem_ends = jm ? jm->smem_ends : ds->smem_ends;
+    a.smem_kstate = ds->smem_kstate;
+    if (jm) {
+        a.slots = jm->slots;
+        rc = hs::jit_launch(*jm, a, grid, stream, &err);
+    } else {
+        rc = hs::launch_eval(*ds, !p.uniform_comm, a, grid, stream, &err);
+    }
     if (rc) return set_err(rc, err);
     return HS_OK;
 }
@@ -247,6 +279,55 @@ int hs_plan_create(const hs_instance_desc *desc, hs_plan **out) {
 }
 
 void hs_plan_destroy(hs_plan *plan) { delete plan; }
+
+int hs_plan_specialize(const hs_plan *plan, double *compile_ms) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    const hs::Plan &p = plan->p;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaFree(nullptr));  // make sure the primary context exists
+    {
+        std::lock_guard<std::mutex> lk(p.mu);
+        if ((int)p.jits.size() > dev && p.jits[dev]) {
+            if (compile_ms) *compile_ms = p.jits[dev]->compile_ms;
+            return HS_OK;
+        }
+    }
+    if (!hs::jit_eligible(p))
+        return set_err(HS_EINVAL, "plan not eligible for the specialised "
+                                  "evaluator (needs K <= 4, one bandwidth over "
+                                  "a full mesh, no capacity / batch-size / "
+                                  "missing-entry / NaN cases)");
+    hs::JitModule *m = nullptr;
+    std::string err;
+    int rc = hs::jit_build(p, dev, &m, &err);
+    if (rc) return set_err(rc, err);
+    std::lock_guard<std::mutex> lk(p.mu);
+    if ((int)p.jits.size() <= dev) p.jits.resize(dev + 1, nullptr);
+    if (p.jits[dev]) {
+        hs::jit_free(m);
+    } else {
+        p.jits[dev] = m;
+    }
+    if (compile_ms) *compile_ms = p.jits[dev]->compile_ms;
+    return HS_OK;
+}
+
+int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
+                             int64_t cap, int64_t *len) {
+    if (!plan || lanes < 1) return set_err(HS_EINVAL, "bad argument");
+    if (!hs::jit_eligible(plan->p))
+        return set_err(HS_EINVAL, "plan not eligible for the specialised evaluator");
+    std::string src;
+    hs::jit_emit(plan->p, lanes, 20, 48, &src);
+    if (len) *len = int64_t(src.size());
+    if (buf && cap > 0) {
+        const size_t m = std::min<size_t>(src.size(), size_t(cap - 1));
+        std::memcpy(buf, src.data(), m);
+        buf[m] = 0;
+    }
+    return HS_OK;
+}
 
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info) {
     if (!plan || !info) return set_err(HS_EINVAL, "null argument");

@@ -1,0 +1,324 @@
+// Shared between the ahead-of-time evaluator (kernels.cu, nvcc) and the
+// per-graph specialised evaluator (jit.cpp, NVRTC): plain-old-data layouts
+// and the CTA tile driver -- genome staging (TMA bulk copy or on-device
+// generation), per-lane evaluation via a Body, outputs, and the fused
+// first-index argmin. Self-contained: no standard headers under NVRTC.
+#pragma once
+
+typedef long long hs_i64;
+typedef unsigned long long hs_u64;
+typedef unsigned int hs_u32;
+typedef unsigned short hs_u16;
+typedef unsigned char hs_u8;
+
+namespace hsk {
+
+// Byte offsets of the sections of the device plan blob.
+struct DevLayout {
+    hs_i64 node, edge, dur, dur_ok, extra, ctab, bclass, cap, okL;
+    hs_i64 cp_fast, cp_fast_ok, cp_task, cp_pred_off, cp_pred_pos;
+    hs_i64 rc_succ_off, rc_succ, rc_pred_off, rc_pred, rc_order;
+    hs_i64 total;
+    hs_i64 eval_bytes;  // [0, eval_bytes) = evaluator tables, 16-aligned
+};
+
+// One predecessor relaxation: `slot` = the predecessor's end-time slot
+// (element offset in the [slot][lane] array after per-device scaling),
+// `gpos` = its genome position. UNIFORM comm: `c` = om_p / beta; CLASS
+// comm: `crow` = p * n_classes row into ctab.
+struct alignas(16) EdgeRec {
+    int slot;
+    int gpos;
+    union {
+        double c;
+        hs_i64 crow;
+    };
+};
+
+// One placement, in genome order.
+struct alignas(16) NodeRec {
+    int e_begin, e_end;
+    int out_slot;  // -1: nothing reads this end time
+    int pad;
+};
+
+struct Best {
+    double cost;
+    hs_i64 index;
+};
+
+// runtime-uniform feature flags of the evaluator
+enum : hs_u32 {
+    F_MEM = 1u,   // capacity can bind (heuristics.py:98-100)
+    F_OKL = 2u,   // some device lacks batch size L (heuristics.py:96)
+    F_MISS = 4u,  // some (task, dev, L) latency entry is missing
+    F_NAN = 8u,   // a NaN can reach a time: keep the running makespan max
+};
+
+// status codes (include/hetsched_b200.h)
+enum { ST_OK = 0, ST_BATCH = 1, ST_MEMORY = 2, ST_LINK = 3, ST_MISSING = 4,
+       ST_GENE = 5 };
+
+struct EvalParams {
+    const hs_u8 *blob;  // device plan blob
+    DevLayout lay;
+    hs_i64 eval_bytes;
+    int V, K;
+    hs_u32 flags;
+    int plan_smem;
+    int lanes, ld_s, slots;
+    int bulk;           // genome tiles may use cp.async.bulk
+    const hs_u8 *genes;
+    hs_i64 n, ld;
+    int gen;            // 1 hash-random, 2 enumerate (K6); 0 staged genes
+    hs_u64 seed;
+    hs_i64 first;
+    const hs_u8 *tmpl;  // [V] fixed genes where group < 0
+    const short *group; // [V] group per position (null: identity)
+    int n_groups;
+    double *makespan;
+    hs_u8 *status;
+    double *starts;     // trace [n][V]
+    hs_u8 *genes_out;   // [n][V]
+    Best *best;
+    Best *partial;      // [grid]
+    hs_u32 *ticket;
+    hs_i64 index_base;
+    hs_i64 smem_tile;   // byte offsets in shared memory: genome tile,
+    hs_i64 smem_ends;   // [slot][lane] end times,
+    hs_i64 smem_kstate; // [2K][lane] device state (generic K)
+};
+
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+
+__device__ __forceinline__ double kinf() { return __longlong_as_double(0x7ff0000000000000ll); }
+__device__ __forceinline__ double knan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+__device__ __forceinline__ double pymax(double a, double b) {
+    return b > a ? b : a;  // Python max(a, b): a unless b > a
+}
+
+// branch-free select (kept as FSEL pairs: the specialised code relies on it
+// to stay divergence free when lanes map tasks to different devices)
+__device__ __forceinline__ double dsel(bool p, double a, double b) {
+    double r;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f64 %0, %1, %2, q;\n}"
+        : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
+    return r;
+}
+
+__device__ __forceinline__ bool best_less(double c1, hs_i64 i1, double c2, hs_i64 i2) {
+    return c1 < c2 || (c1 == c2 && i1 < i2);
+}
+
+__device__ __forceinline__ hs_u64 splitmix64(hs_u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ hs_u32 smem_addr(const void *p) {
+    return (hs_u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(hs_u64 *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// TMA 1-D bulk copy global -> shared, completion on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, hs_u32 bytes,
+                                         hs_u64 *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(hs_u64 *bar, hs_u32 phase) {
+    asm volatile("{\n"
+                 ".reg .pred p;\n"
+                 "WAIT_%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "@!p bra WAIT_%=;\n"
+                 "}\n" ::"r"(smem_addr(bar)), "r"(phase) : "memory");
+}
+
+// lexicographic (cost, index) min across the CTA, then across CTAs through
+// `partial` + a ticket: the last CTA to finish writes *best.
+__device__ __forceinline__ void warp_best(double &bc, hs_i64 &bi) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oc = __shfl_down_sync(0xffffffffu, bc, o);
+        const hs_i64 oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (best_less(oc, oi, bc, bi)) {
+            bc = oc;
+            bi = oi;
+        }
+    }
+}
+
+static __device__ __noinline__ void reduce_best(double bc, hs_i64 bi, Best *partial,
+                                         hs_u32 *ticket, Best *best) {
+    __shared__ double s_c[32];
+    __shared__ hs_i64 s_i[32];
+    __shared__ int s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = (blockDim.x + 31) >> 5;
+    warp_best(bc, bi);
+    if (lane == 0) {
+        s_c[warp] = bc;
+        s_i[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w)
+            if (best_less(s_c[w], s_i[w], bc, bi)) {
+                bc = s_c[w];
+                bi = s_i[w];
+            }
+        partial[blockIdx.x].cost = bc;
+        partial[blockIdx.x].index = bi;
+        __threadfence();
+        const hs_u32 t = atomicAdd(ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    bc = kinf();
+    bi = 0x7fffffffffffffffll;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        const double c = ((volatile double *)&partial[b].cost)[0];
+        const hs_i64 i = ((volatile hs_i64 *)&partial[b].index)[0];
+        if (best_less(c, i, bc, bi)) {
+            bc = c;
+            bi = i;
+        }
+    }
+    warp_best(bc, bi);
+    __syncthreads();
+    if (lane == 0) {
+        s_c[warp] = bc;
+        s_i[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w)
+            if (best_less(s_c[w], s_i[w], bc, bi)) {
+                bc = s_c[w];
+                bi = s_i[w];
+            }
+        best->cost = bc;
+        best->index = bi == 0x7fffffffffffffffll ? -1 : bi;
+        *ticket = 0;  // reusable by the next launch on this stream
+    }
+}
+
+// K6: on-device candidate rows (oracle/hs_oracle.py::gen_genes, or
+// mixed-radix enumeration), expanded over the group map.
+__device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 cidx) {
+    const int NG = a.n_groups, K = a.K, V = a.V;
+    const hs_u64 c = (hs_u64)cidx;
+    if (a.gen == 1) {
+        const int W4 = (NG + 3) >> 2;
+        hs_u32 *row = reinterpret_cast<hs_u32 *>(r8);
+        for (int w = 0; w < W4; ++w) {
+            const hs_u64 ctr = c * (hs_u64)W4 + (hs_u64)w + 1ull;
+            const hs_u64 h = splitmix64(a.seed + ctr * 0x9E3779B97F4A7C15ull);
+            hs_u32 pk = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const hs_u32 v16 = (hs_u32)((h >> (16 * q)) & 0xFFFFull);
+                pk |= ((v16 * (hs_u32)K) >> 16) << (8 * q);
+            }
+            row[w] = pk;
+        }
+    } else if (c < (1ull << 32)) {
+        hs_u32 x = (hs_u32)c;
+        for (int j = 0; j < NG; ++j) {
+            r8[j] = (hs_u8)(x % (hs_u32)K);
+            x /= (hs_u32)K;
+        }
+    } else {
+        hs_u64 x = c;
+        for (int j = 0; j < NG; ++j) {
+            r8[j] = (hs_u8)(x % (hs_u64)K);
+            x /= (hs_u64)K;
+        }
+    }
+    if (a.group) {
+        // group ids are numbered by first position (group[p] <= p), so a
+        // backward sweep expands the compact values in place
+        for (int q = V - 1; q >= 0; --q) {
+            const int gq = a.group[q];
+            r8[q] = gq < 0 ? a.tmpl[q] : r8[gq];
+        }
+    }
+}
+
+// The CTA tile loop. `body.run(row, lane, cand, valid, ms, st)` evaluates
+// the lane's candidate from its staged genome row.
+template <class Body>
+__device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Body &body) {
+    hs_u64 *bar = reinterpret_cast<hs_u64 *>(smem);
+    hs_u8 *gtile = smem + a.smem_tile;
+    const int T = blockDim.x, tid = threadIdx.x;
+    const int lanes = a.lanes;
+    if (tid == 0) mbar_init(bar);
+    __syncthreads();
+    double bc = kinf();
+    hs_i64 bi = 0x7fffffffffffffffll;
+    hs_u32 phase = 0;
+    const hs_i64 ntiles = (a.n + lanes - 1) / lanes;
+    for (hs_i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const hs_i64 c0 = tile * lanes;
+        const hs_i64 left = a.n - c0;
+        const int rows = left < lanes ? (int)left : lanes;
+        __syncthreads();  // the previous tile's genomes are no longer read
+        if (a.gen) {
+            if (tid < rows) {
+                hs_u8 *r8 = gtile + (hs_i64)tid * a.ld_s;
+                gen_row(a, r8, a.first + c0 + tid);
+                if (a.genes_out) {
+                    hs_u8 *o = a.genes_out + (c0 + tid) * (hs_i64)a.V;
+                    for (int i = 0; i < a.V; ++i) o[i] = r8[i];
+                }
+            }
+        } else {
+            const hs_i64 bytes = (hs_i64)rows * a.ld;
+            const hs_u8 *src = a.genes + c0 * a.ld;
+            if (a.bulk && bytes > 0 && (bytes & 15) == 0) {
+                if (tid == 0) bulk_g2s(gtile, src, (hs_u32)bytes, bar);
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+            } else {
+                for (hs_i64 b = tid; b < bytes; b += T) gtile[b] = src[b];
+            }
+        }
+        __syncthreads();
+        const int li = tid;
+        const hs_i64 cand = c0 + li;
+        const bool valid = li < rows;
+        double ms;
+        int st;
+        body.run(gtile + (hs_i64)li * a.ld_s, li, cand, valid, ms, st);
+        if (valid) {
+            if (a.makespan) a.makespan[cand] = ms;
+            if (a.status) a.status[cand] = (hs_u8)st;
+            const double key = (ms != ms) ? kinf() : ms;
+            const hs_i64 gidx = a.index_base + cand;
+            if (best_less(key, gidx, bc, bi)) {
+                bc = key;
+                bi = gidx;
+            }
+        }
+    }
+    if (a.best) reduce_best(bc, bi, a.partial, a.ticket, a.best);
+}
+
+#endif  // device code
+
+}  // namespace hsk

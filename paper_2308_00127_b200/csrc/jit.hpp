@@ -1,0 +1,31 @@
+// Per-graph specialised evaluator (jit.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "eval_common.cuh"
+#include "plan.hpp"
+
+namespace hs {
+
+struct JitModule {
+    int device = -1;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
+    size_t smem = 0;
+    int64_t smem_tile = 0, smem_ends = 0;
+    size_t src_bytes = 0;
+    double compile_ms = 0.0;
+};
+
+bool jit_eligible(const Plan &p);
+int jit_emit(const Plan &p, int T, int reg_budget, int reg_window, std::string *src);
+int jit_build(const Plan &p, int device, JitModule **out, std::string *err);
+void jit_free(JitModule *m);
+int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid,
+               cudaStream_t stream, std::string *err);
+
+}  // namespace hs

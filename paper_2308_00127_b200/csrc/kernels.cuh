@@ -1,4 +1,4 @@
-// Kernel parameter blocks and launchers (kernels.cu), used by capi.cu.
+// Launchers of the ahead-of-time kernels (kernels.cu), used by capi.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -6,46 +6,16 @@
 #include <cstdint>
 #include <string>
 
+#include "eval_common.cuh"
 #include "plan.hpp"
 
 namespace hs {
 
-// runtime-uniform feature flags of the evaluator
-enum : uint32_t {
-    F_MEM = 1u,   // capacity can bind (heuristics.py:98-100)
-    F_OKL = 2u,   // some device lacks batch size L (heuristics.py:96)
-    F_MISS = 4u,  // some (task, dev, L) latency entry is missing
-    F_NAN = 8u,   // a NaN can reach a time: keep the running makespan max
-};
-
-struct EvalParams {
-    const uint8_t *blob;  // device plan blob (slots pre-scaled by lanes)
-    DevLayout lay;
-    int64_t eval_bytes;
-    int V, K;
-    uint32_t flags;
-    int plan_smem;
-    int lanes, ld_s, slots;
-    int bulk;             // genome tiles may use cp.async.bulk
-    // candidates
-    const uint8_t *genes;
-    int64_t n, ld;
-    int gen;              // 1: hash-random, 2: enumerate (K6); 0: staged genes
-    uint64_t seed;
-    int64_t first;
-    const uint8_t *tmpl;  // [V] fixed genes where group < 0
-    const int16_t *group; // [V] group per position (null: identity)
-    int n_groups;
-    // outputs (each may be null)
-    double *makespan;
-    uint8_t *status;
-    double *starts;       // trace: [n][V]
-    uint8_t *genes_out;   // gen: [n][V]
-    hs_best *best;
-    hs_best *partial;     // [grid]
-    unsigned int *ticket;
-    int64_t index_base;
-};
+using hsk::EvalParams;
+using hsk::F_MEM;
+using hsk::F_MISS;
+using hsk::F_NAN;
+using hsk::F_OKL;
 
 int eval_occupancy(int kt, bool cls, int T, size_t smem, int *blocks);
 int launch_eval(const DevState &ds, bool cls, const EvalParams &p, int grid,

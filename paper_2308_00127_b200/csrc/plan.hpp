@@ -9,45 +9,21 @@
 #include <vector>
 
 #include "../../include/hetsched_b200.h"
+#include "eval_common.cuh"
 
 namespace hs {
 
 constexpr uint8_t kNoLink = 255;   // comm class of a missing link
 constexpr int kMaxRegK = 4;        // K <= 4: per-device state in registers
 
-// One predecessor relaxation. `slot` is the predecessor's live end-time
-// slot, `gpos` its genome position (to read its gene). UNIFORM comm:
-// `c` = om_p / beta. CLASS comm: `crow` = p * n_classes row into ctab.
-struct alignas(16) EdgeRec {
-    int32_t slot;
-    int32_t gpos;
-    union {
-        double c;
-        int64_t crow;
-    };
-};
+using hsk::DevLayout;
+using hsk::EdgeRec;
+using hsk::NodeRec;
 static_assert(sizeof(EdgeRec) == 16, "EdgeRec layout");
-
-// One placement, in genome order.
-struct alignas(16) NodeRec {
-    int32_t e_begin, e_end;  // EdgeRec range
-    int32_t out_slot;        // -1: no successor reads this end time
-    int32_t pad;
-};
 static_assert(sizeof(NodeRec) == 16, "NodeRec layout");
 
 struct DevState;
-
-// Byte offsets of the sections of the device blob.
-struct DevLayout {
-    int64_t node, edge, dur, dur_ok, extra, ctab, bclass, cap, okL;
-    int64_t cp_fast, cp_fast_ok, cp_task, cp_pred_off, cp_pred_pos;
-    int64_t rc_succ_off, rc_succ, rc_pred_off, rc_pred, rc_order;
-    int64_t total;
-    // size of the per-CTA shared staging of the evaluator's plan part
-    // (node .. okL), 16-aligned
-    int64_t eval_bytes;
-};
+struct JitModule;
 
 struct Plan {
     // ---- description
@@ -90,6 +66,7 @@ struct Plan {
     // ---- lazily uploaded per-device state
     mutable std::mutex mu;
     mutable std::vector<DevState *> devs;  // index = device ordinal
+    mutable std::vector<JitModule *> jits;  // index = device ordinal
 
     int pref_ld() const {
         // genome row stride with an odd number of 32-bit words: lane-strided
@@ -111,6 +88,7 @@ struct DevState {
     int blocks_per_sm = 0, sms = 0;
     bool plan_smem = false;
     size_t smem = 0;          // dynamic shared memory per CTA
+    int64_t smem_tile = 0, smem_ends = 0, smem_kstate = 0;
     int kt = 0;               // K template (2,3,4) or 0 = generic K
 };
 
@@ -119,5 +97,8 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err);
 
 // Device state for the current device (configures + uploads on first use).
 int get_dev_state(const Plan &p, const DevState **out, std::string *err);
+
+// Specialised module of the plan for `dev`, or null (HS_JIT=0 disables).
+const JitModule *find_jit(const Plan &p, int dev);
 
 }  // namespace hs

@@ -182,6 +182,7 @@ def fitness_batch(genes, g, hw, table, L: int, *,
                                                genes.stride(1) != 1):
             raise GraphError("genes must be a uint8 [n, >=V] row-major tensor")
         n = genes.shape[0]
+        plan.maybe_specialize(n)
         ms = torch.empty(n, dtype=torch.float64, device=genes.device)
         st = torch.empty(n, dtype=torch.uint8, device=genes.device)
         plan.eval(genes, ms, st, None, index_base)
@@ -203,6 +204,7 @@ def fitness_batch(genes, g, hw, table, L: int, *,
         genes = np.where((genes < 0) | (genes > 255), 255,
                          genes).astype(np.uint8)
     n = genes.shape[0]
+    plan.maybe_specialize(n)
     ms = np.empty(n, np.float64)
     st = np.empty(n, np.uint8)
     plan.eval_host(genes, ms, st, None, index_base)
@@ -211,6 +213,12 @@ def fitness_batch(genes, g, hw, table, L: int, *,
     if n and st.max() >= N.ST_MISSING:
         _raise_status(int(st[np.argmax(st >= N.ST_MISSING)]))
     return ms
+
+
+def specialize(g, hw, table, L: int, order=None) -> float:
+    """Compile the graph-specialised evaluator for this instance on the
+    current device (csrc/jit.cpp); returns the compile time in ms."""
+    return get_plan(g, hw, table, L, order).specialize()
 
 
 def throughput(makespan, L: int):
@@ -228,6 +236,7 @@ def argmin_batch(genes, g, hw, table, L: int, *,
     """(makespan, index) of the first best genome (numpy.argmin semantics,
     +inf allowed) computed by the fused on-device reduction."""
     plan = get_plan(g, hw, table, L, order)
+    plan.maybe_specialize(int(genes.shape[0]))
     if hasattr(genes, "data_ptr"):
         import torch
         best = torch.empty(2, dtype=torch.int64, device=genes.device)
@@ -246,6 +255,7 @@ def random_search(g, hw, table, L: int, n: int, *, seed: int = 0,
     c in [first, first + n)) and return (best makespan, index, genome)."""
     import torch
     plan = get_plan(g, hw, table, L)
+    plan.maybe_specialize(n)
     bests = []
     dbest = torch.empty(2, dtype=torch.int64, device="cuda")
     for lo in range(first, first + n, chunk):

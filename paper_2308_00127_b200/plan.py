@@ -121,6 +121,55 @@ class Plan:
         self.words = info.words
         self._reach = None
         self._lock = threading.Lock()
+        self.specialized_ms = None
+
+    # ------------------------------------------------------- specialisation
+    def specialize(self) -> float:
+        """Compile the graph-specialised evaluator for the current device
+        (NVRTC, once per plan and device); returns the compile time in ms.
+        Raises GraphError when the plan is outside its scope."""
+        import torch
+        torch.cuda.init()
+        ms = C.c_double()
+        N.check(self._lib.hs_plan_specialize(self.handle, C.byref(ms)),
+                "specialize")
+        self.specialized_ms = ms.value
+        return ms.value
+
+    def maybe_specialize(self, n: int) -> bool:
+        """Specialise when a batch is large enough to amortise the compile
+        (HS_JIT_MIN candidates, default 2**20); False if out of scope."""
+        import os
+        if self.specialized_ms is not None:
+            return True
+        if os.environ.get("HS_JIT", "1") == "0":
+            return False
+        if n < int(os.environ.get("HS_JIT_MIN", 1 << 20)):
+            return False
+        if not self.jit_eligible():
+            return False
+        self.specialize()
+        return True
+
+    def jit_eligible(self) -> bool:
+        i = self.info
+        return bool(self.K <= 4 and i.uniform_comm and not i.mem_check and
+                    i.all_batch_ok and i.latency_complete and self.V > 0 and
+                    self._no_nan())
+
+    def _no_nan(self) -> bool:
+        n = C.c_int64()
+        return self._lib.hs_plan_emit_specialized(self.handle, 32, None, 0,
+                                                  C.byref(n)) == 0
+
+    def specialized_source(self, lanes: int = 192) -> str:
+        n = C.c_int64()
+        N.check(self._lib.hs_plan_emit_specialized(self.handle, lanes, None, 0,
+                                                   C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        N.check(self._lib.hs_plan_emit_specialized(self.handle, lanes, buf,
+                                                   n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -10,6 +10,8 @@ for name in sys.argv[1:] or ["ws200"]:
     doc = json.load(open(f"tests/golden/instances/{name}.json"))
     g, hw, t = hs.load_instance(doc)
     plan = get_plan(g, hw, t, 1)
+    if os.environ.get("QP_JIT", "1") == "1" and plan.jit_eligible():
+        print("specialize ms", plan.specialize())
     n = int(os.environ.get("QP_N", 1 << 22))
     ld = plan.pref_ld
     genes = torch.randint(0, plan.K, (n, ld), dtype=torch.uint8, device="cuda")
