@@ -96,6 +96,7 @@ typedef struct hs_plan_info {
     int32_t words;                /* ceil(n_tasks/64) for masks / bitsets */
     int32_t pref_ld;              /* genome row stride that makes the staged
                                      tile bank-conflict free (>= V) */
+    int32_t specializable;        /* hs_plan_specialize can serve this plan */
 } hs_plan_info;
 
 typedef struct hs_best {

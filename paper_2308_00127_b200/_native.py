@@ -49,7 +49,7 @@ class PlanInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "V", "E", "K", "L", "live_slots", "n_classes", "uniform_comm",
         "full_mesh", "mem_check", "all_batch_ok", "latency_complete", "words",
-        "pref_ld")]
+        "pref_ld", "specializable")]
 
 
 class Best(C.Structure):

@@ -245,7 +245,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.index_base = index_base;
     a.smem_tile = jm ? jm->smem_tile : ds->smem_tile;
     a.smem_ends = jm ? jm->smem_ends : ds->smem_ends;
-    a.smem_kstate = ds->smem_kstate;
+    a.smem_kstate = jm ? jm->smem_kstate : ds->smem_kstate;
     if (jm) {
         a.slots = jm->slots;
         rc = hs::jit_launch(*jm, a, grid, stream, &err);
@@ -319,7 +319,7 @@ int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
     if (!hs::jit_eligible(plan->p))
         return set_err(HS_EINVAL, "plan not eligible for the specialised evaluator");
     std::string src;
-    hs::jit_emit(plan->p, lanes, 20, 48, &src);
+    hs::jit_emit(plan->p, lanes, hs::JitOpts::from_env(), &src);
     if (len) *len = int64_t(src.size());
     if (buf && cap > 0) {
         const size_t m = std::min<size_t>(src.size(), size_t(cap - 1));
@@ -345,6 +345,7 @@ int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info) {
     info->latency_complete = p.latency_complete;
     info->words = p.words;
     info->pref_ld = p.pref_ld();
+    info->specializable = hs::jit_eligible(p) ? 1 : 0;
     return HS_OK;
 }
 

@@ -95,15 +95,42 @@ std::string sel(const std::string &d, const std::vector<std::string> &vals) {
 
 }  // namespace
 
+JitOpts JitOpts::from_env() {
+    JitOpts o;
+    const char *env = getenv("HS_JIT_OPTS");
+    if (!env) return o;
+    std::string s(env);
+    size_t at = 0;
+    while (at < s.size()) {
+        size_t end = s.find(',', at);
+        if (end == std::string::npos) end = s.size();
+        const std::string kv = s.substr(at, end - at);
+        const size_t eq = kv.find('=');
+        if (eq != std::string::npos) {
+            const std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+            if (k == "regs") o.reg_budget = std::atoi(v.c_str());
+            if (k == "win") o.reg_window = std::atoi(v.c_str());
+            if (k == "avail") o.avail_smem = v == "smem";
+            if (k == "dur") o.dur_smem = v == "smem";
+        }
+        at = end + 1;
+    }
+    return o;
+}
+
+static int64_t dur_bytes(const Plan &p) {
+    return (int64_t(p.V) * p.K * 8 + 15) & ~int64_t(15);
+}
+
 bool jit_eligible(const Plan &p) {
     return p.K <= 4 && p.uniform_comm && !p.mem_check && p.all_batch_ok &&
            p.latency_complete && !p.nan_possible && p.V > 0;
 }
 
 // Emits the body for T lanes. Returns the number of shared-memory slots.
-int jit_emit(const Plan &p, int T, int reg_budget, int reg_window,
-             std::string *src) {
+int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     const int V = p.V, K = p.K;
+    const int reg_budget = o.reg_budget, reg_window = o.reg_window;
     // lifetimes in genome order
     std::vector<int> last(V, -1);
     std::vector<std::vector<int>> preds(V);  // positions
@@ -142,11 +169,19 @@ int jit_emit(const Plan &p, int T, int reg_budget, int reg_window,
         std::string &s = *src;
         s.clear();
         s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
-        s += "struct JitBody {\n  double *ends; double *starts;\n";
+        s += "struct JitBody {\n  double *ends; double *avail; const double *dur; "
+             "double *starts;\n";
         s += "  __device__ __forceinline__ void run(const hs_u8 *g, int li, "
              "hs_i64 cand, bool valid, double &ms_out, int &st_out) {\n";
         s += "    double *E = ends + li;\n";
-        for (int k = 0; k < K; ++k) s += "    double a" + std::to_string(k) + " = 0.0;\n";
+        if (o.avail_smem) {
+            s += "    double *A = avail + li;\n";
+            for (int k = 0; k < K; ++k)
+                s += "    A[" + std::to_string(k * T) + "] = 0.0;\n";
+        } else {
+            for (int k = 0; k < K; ++k)
+                s += "    double a" + std::to_string(k) + " = 0.0;\n";
+        }
         s += "    int gmax = 0;\n";
         char buf[1024];
         for (int i = 0; i < V; ++i) {
@@ -204,23 +239,38 @@ int jit_emit(const Plan &p, int T, int reg_budget, int reg_window,
                 du.push_back(lit(p.dur[size_t(i) * K + k]));
             }
             const std::string si = "s" + std::to_string(i);
-            s += "    const double " + si + " = pymax(" + r + ", " + sel(di, av) + ");\n";
+            const std::string Ai = "A" + std::to_string(i);
+            if (o.avail_smem) {
+                s += "    double *" + Ai + " = A + " + di + " * " + std::to_string(T) + ";\n";
+                s += "    const double " + si + " = pymax(" + r + ", *" + Ai + ");\n";
+            } else {
+                s += "    const double " + si + " = pymax(" + r + ", " + sel(di, av) + ");\n";
+            }
+            std::string dsrc = sel(di, du);
+            if (o.dur_smem && dsrc != du[0])
+                dsrc = "dur[" + std::to_string(i * K) + " + " + di + "]";
             const std::string ei = "e" + std::to_string(i);
-            s += "    const double " + ei + " = " + si + " + " + sel(di, du) + ";\n";
+            s += "    const double " + ei + " = " + si + " + " + dsrc + ";\n";
             std::snprintf(buf, sizeof buf,
                           "    if (starts && valid) starts[cand * %d + %d] = %s;\n", V, i,
                           si.c_str());
             s += buf;
             if (where[i] >= 0)
                 s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + ei + ";\n";
-            for (int k = 0; k < K; ++k) {
-                const std::string a = "a" + std::to_string(k);
-                s += "    " + a + " = dsel(" + di + " == " + std::to_string(k) + ", " + ei +
-                     ", " + a + ");\n";
+            if (o.avail_smem) {
+                s += "    *" + Ai + " = " + ei + ";\n";
+            } else {
+                for (int k = 0; k < K; ++k) {
+                    const std::string a = "a" + std::to_string(k);
+                    s += "    " + a + " = dsel(" + di + " == " + std::to_string(k) + ", " +
+                         ei + ", " + a + ");\n";
+                }
             }
         }
         s += "    double ms = 0.0;\n";
-        for (int k = 0; k < K; ++k) s += "    ms = pymax(ms, a" + std::to_string(k) + ");\n";
+        for (int k = 0; k < K; ++k)
+            s += o.avail_smem ? "    ms = pymax(ms, A[" + std::to_string(k * T) + "]);\n"
+                              : "    ms = pymax(ms, a" + std::to_string(k) + ");\n";
         std::snprintf(buf, sizeof buf,
                       "    const int st = gmax >= %d ? ST_GENE : ST_OK;\n"
                       "    ms_out = st ? knan() : ms;\n    st_out = st;\n  }\n};\n", K);
@@ -231,9 +281,19 @@ int jit_emit(const Plan &p, int T, int reg_budget, int reg_window,
                       "  extern __shared__ __align__(16) hs_u8 smem[];\n"
                       "  JitBody body;\n"
                       "  body.ends = reinterpret_cast<double *>(smem + a.smem_ends);\n"
-                      "  body.starts = a.starts;\n"
-                      "  eval_tiles(a, smem, body);\n}\n", T);
+                      "  body.avail = reinterpret_cast<double *>(smem + a.smem_kstate);\n"
+                      "  body.dur = reinterpret_cast<const double *>(smem + 16);\n"
+                      "  body.starts = a.starts;\n", T);
         s += buf;
+        if (o.dur_smem) {
+            std::snprintf(buf, sizeof buf,
+                          "  { const uint4 *src = reinterpret_cast<const uint4 *>(a.blob + "
+                          "a.lay.dur);\n    uint4 *dst = reinterpret_cast<uint4 *>(smem + 16);\n"
+                          "    for (int q = threadIdx.x; q < %lld; q += blockDim.x) dst[q] = "
+                          "src[q]; }\n", (long long)(dur_bytes(p) / 16));
+            s += buf;
+        }
+        s += "  eval_tiles(a, smem, body);\n}\n";
         return next;
     }
 }
@@ -252,18 +312,19 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     int optin = 0, sms = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const int reg_budget = 20, reg_window = 48;
-    const int slots = jit_emit(p, 32, reg_budget, reg_window, nullptr);
+    const JitOpts o = JitOpts::from_env();
+    const int slots = jit_emit(p, 32, o, nullptr);
     const int ld_cap = p.pref_ld() + 16;
-    const int64_t per_lane = ld_cap + int64_t(slots) * 8;
-    const int64_t budget = int64_t(optin) - 16 - 1024;
+    const int64_t per_lane = ld_cap + int64_t(slots) * 8 + (o.avail_smem ? 8 * p.K : 0);
+    const int64_t head = 16 + (o.dur_smem ? dur_bytes(p) : 0);
+    const int64_t budget = int64_t(optin) - head - 1024;
     int T = int(std::min<int64_t>(budget / per_lane, 256) / 32 * 32);
     if (T < 32) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
     }
     std::string src;
-    jit_emit(p, T, reg_budget, reg_window, &src);
+    jit_emit(p, T, o, &src);
     const char *hdr_src[] = {kEvalCommonSrc};
     const char *hdr_name[] = {"eval_common.cuh"};
     nvrtcProgram_t prog = nullptr;
@@ -294,9 +355,11 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->T = m->lanes = T;
     m->slots = slots;
     m->ld_cap = ld_cap;
-    m->smem_tile = 16;
-    m->smem_ends = 16 + ((int64_t(T) * ld_cap + 15) & ~int64_t(15));
-    m->smem = size_t(m->smem_ends + int64_t(slots) * T * 8);
+    m->opts = o;
+    m->smem_tile = head;
+    m->smem_ends = head + ((int64_t(T) * ld_cap + 15) & ~int64_t(15));
+    m->smem_kstate = m->smem_ends + int64_t(slots) * T * 8;
+    m->smem = size_t(m->smem_kstate + (o.avail_smem ? int64_t(8) * p.K * T : 0));
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0,
                                         nullptr, nullptr, 0);
     if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern, m->lib, "hs_jit_eval");

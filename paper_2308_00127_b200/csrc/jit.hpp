@@ -10,19 +10,30 @@
 
 namespace hs {
 
+// Code-generation choices (HS_JIT_OPTS="regs=20,win=48,avail=reg,dur=sel")
+struct JitOpts {
+    int reg_budget = 20;   // end times kept in registers at once
+    int reg_window = 48;   // ... when consumed within this many positions
+    bool avail_smem = false;  // per-device available times in shared memory
+    bool dur_smem = false;    // latency table in shared memory (else selects)
+    static JitOpts from_env();
+};
+
 struct JitModule {
     int device = -1;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;
-    int64_t smem_tile = 0, smem_ends = 0;
+    int64_t smem_tile = 0, smem_ends = 0, smem_kstate = 0;
+    JitOpts opts;
     size_t src_bytes = 0;
     double compile_ms = 0.0;
 };
 
 bool jit_eligible(const Plan &p);
-int jit_emit(const Plan &p, int T, int reg_budget, int reg_window, std::string *src);
+// Emits the kernel for T lanes; returns the number of shared-memory slots.
+int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src);
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err);
 void jit_free(JitModule *m);
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid,

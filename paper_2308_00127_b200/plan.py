@@ -152,15 +152,8 @@ class Plan:
         return True
 
     def jit_eligible(self) -> bool:
-        i = self.info
-        return bool(self.K <= 4 and i.uniform_comm and not i.mem_check and
-                    i.all_batch_ok and i.latency_complete and self.V > 0 and
-                    self._no_nan())
-
-    def _no_nan(self) -> bool:
-        n = C.c_int64()
-        return self._lib.hs_plan_emit_specialized(self.handle, 32, None, 0,
-                                                  C.byref(n)) == 0
+        """Inside the specialised evaluator's scope (csrc/jit.cpp)."""
+        return bool(self.info.specializable)
 
     def specialized_source(self, lanes: int = 192) -> str:
         n = C.c_int64()
