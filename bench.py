@@ -167,6 +167,39 @@ def c_port_rate(doc, cores):
     return len(genes) / (time.perf_counter() - t0)
 
 
+def time_to_solution(doc_name="ws_stack_10x20", budget=2000, seed=0):
+    """Heuristic time-to-solution: the reference's SA and (1+1) EA
+    (heuristics.py:259-334) on the WS 10x20 stack, GPU-batched (this repo)
+    vs the CPU restatement that evaluates one candidate per step like the
+    reference (oracle/hs_search.py). Both must end on the same genome."""
+    import paper_2308_00127_b200 as hs
+    from oracle import hs_oracle as O
+    from oracle import hs_search as S
+    with open(os.path.join(ROOT, "tests", "golden", "instances",
+                           doc_name + ".json")) as f:
+        doc = json.load(f)
+    g, hw, t = hs.load_instance(doc)
+    inst = O.Instance.from_doc(doc)
+    out = {}
+    for algo in ("sa", "ea"):
+        hs.fitness(hs.genome_from_map(g, hw, {i: sorted(hw.devices)[0]
+                                              for i in g.tasks}), g, hw, t, 1)
+        t0 = time.perf_counter()
+        s = (hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=budget)
+             if algo == "sa" else
+             hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=budget))
+        gpu_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fit, _ = (S.simulated_annealing(inst, 1, seed, budget) if algo == "sa"
+                  else S.one_plus_one_ea(inst, 1, seed, budget))
+        cpu_s = time.perf_counter() - t0
+        out[f"{algo}_{doc_name}_budget{budget}"] = {
+            "gpu_s": gpu_s, "cpu_port_s": cpu_s, "speedup": cpu_s / gpu_s,
+            "objective_ms": s.objective, "same_result": s.objective == fit,
+            "cpu": "oracle/hs_search.py, 1 core, one candidate per step"}
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -203,6 +236,7 @@ def main():
                     help="candidates per GPU per step")
     ap.add_argument("--e2e-n", type=int, default=1 << 23)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-jit", action="store_true",
                     help="time the ahead-of-time kernel instead of the "
                          "graph-specialised one")
@@ -343,6 +377,13 @@ def main():
             dist.destroy_process_group()
         return
 
+    tts = None
+    if not args.no_tts:
+        try:
+            tts = time_to_solution()
+        except Exception as exc:  # reported, never fatal for the bench
+            tts = {"error": repr(exc)}
+
     cpu = None
     if not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
@@ -370,7 +411,7 @@ def main():
                      "kernel_ms": kern_ms,
                      "kernel": "hs_jit_eval" if jit_ms is not None
                      else "hs::eval_kernel"},
-        "cpu_baseline": cpu, "e2e": e2e,
+        "cpu_baseline": cpu, "e2e": e2e, "time_to_solution": tts,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }

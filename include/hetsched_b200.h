@@ -116,7 +116,8 @@ int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
  * cost, reported in *compile_ms); later hs_eval* calls on this device use
  * it. HS_EINVAL when the plan is outside the specialised scope (K <= 4,
  * one bandwidth over a full mesh, no capacity / batch-size / missing-entry
- * / NaN cases); the ahead-of-time kernel then keeps serving the plan. */
+ * / NaN cases, V <= 512, E <= 2048); the ahead-of-time kernel then keeps
+ * serving the plan. */
 int hs_plan_specialize(const hs_plan *plan, double *compile_ms);
 /* The CUDA source the specialiser would compile for `lanes` lanes. */
 int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
@@ -174,6 +175,17 @@ int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,
 /* Descendant / ancestor bitsets [n_tasks x words] (task insertion index). */
 int hs_reach(const hs_plan *plan, uint64_t *d_desc, uint64_t *d_anc,
              void *stream);
+
+/* Newman modularity (resolution gamma) of P partitions of the graph's
+ * undirected shadow: d_labels int32 [P x n_tasks] community index per task
+ * (insertion order), communities 0..n_comm-1 summed in index order, same
+ * binary64 sequence as networkx.community.modularity. The split
+ * heuristic's module partition (splitting.py:178-219) is one such
+ * partition; the reference itself computes no score.
+ * d_status[k] = 1 when a label is out of range. */
+int hs_modularity(const hs_plan *plan, const int32_t *d_labels, int64_t P,
+                  int32_t n_comm, double resolution, double *d_out,
+                  uint8_t *d_status, void *stream);
 
 /* host: lexicographic (cost, index) minimum of n bests */
 int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out);

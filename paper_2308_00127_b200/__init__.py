@@ -21,5 +21,7 @@ from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
                      dep_subgraph, lower_bound, pre_subgraph)
 from .splitting import ModuleSolver, gpu_module_solver
+from .modularity import (decomposition_modularity, modularity,
+                         modularity_batch)
 
 __version__ = "0.1.0"

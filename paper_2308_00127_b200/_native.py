@@ -94,6 +94,8 @@ def load() -> C.CDLL:
             "hs_trace": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, vp]),
             "hs_cp_bound": (C.c_int, [vp, vp, i64, vp, vp, vp]),
             "hs_reach": (C.c_int, [vp, vp, vp, vp]),
+            "hs_modularity": (C.c_int, [vp, vp, i64, i32, C.c_double, vp, vp,
+                                        vp]),
             "hs_best_merge": (C.c_int, [_p(Best), i64, _p(Best)]),
         }
         for name, (res, args) in sig.items():
@@ -112,7 +114,7 @@ def exported_symbols() -> list[str]:
             "hs_plan_destroy", "hs_plan_get_info", "hs_plan_order",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
-            "hs_cp_bound", "hs_reach", "hs_best_merge"]
+            "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge"]
 
 
 def check(rc: int, what: str = "") -> None:

@@ -529,6 +529,32 @@ int hs_reach(const hs_plan *plan, uint64_t *d_desc, uint64_t *d_anc,
     return rc ? set_err(rc, err) : HS_OK;
 }
 
+int hs_modularity(const hs_plan *plan, const int32_t *d_labels, int64_t P,
+                  int32_t n_comm, double resolution, double *d_out,
+                  uint8_t *d_status, void *stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (P < 0 || n_comm < 1 || (P > 0 && (!d_labels || !d_out)))
+        return set_err(HS_EINVAL, "bad partition arguments");
+    const hs::Plan &p = plan->p;
+    if (P == 0) return HS_OK;
+    if (p.E == 0)
+        return set_err(HS_EINVAL, "modularity is undefined without edges");
+    if (int64_t(n_comm) * 16 > 200 * 1024)
+        return set_err(HS_EINVAL, "too many communities");
+    const hs::DevState *ds = nullptr;
+    std::string err;
+    int rc = hs::get_dev_state(p, &ds, &err);
+    if (rc) return set_err(rc, err);
+    // undirected shadow of a DAG without duplicate edges: deg_sum = 2E
+    const double deg_sum = 2.0 * double(p.E);
+    const double m = deg_sum / 2.0;
+    const double norm = 1.0 / (deg_sum * deg_sum);
+    rc = hs::launch_modularity(ds->blob, p.lay, p.NT, d_labels, P, n_comm,
+                               resolution, m, norm, d_out, d_status,
+                               static_cast<cudaStream_t>(stream), &err);
+    return rc ? set_err(rc, err) : HS_OK;
+}
+
 int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out) {
     if (!out || (n > 0 && !bests)) return set_err(HS_EINVAL, "null argument");
     hs_best b{__builtin_huge_val(), -1};

@@ -122,9 +122,14 @@ static int64_t dur_bytes(const Plan &p) {
     return (int64_t(p.V) * p.K * 8 + 15) & ~int64_t(15);
 }
 
+// Straight-line code grows with V + E and ptxas time super-linearly
+// (minutes at V ~ 1000), so very large graphs stay on the AOT kernel.
+constexpr int kJitMaxV = 512, kJitMaxE = 2048;
+
 bool jit_eligible(const Plan &p) {
     return p.K <= 4 && p.uniform_comm && !p.mem_check && p.all_batch_ok &&
-           p.latency_complete && !p.nan_possible && p.V > 0;
+           p.latency_complete && !p.nan_possible && p.V > 0 &&
+           p.V <= kJitMaxV && p.E <= kJitMaxE;
 }
 
 // Emits the body for T lanes. Returns the number of shared-memory slots.

@@ -12,10 +12,11 @@ namespace hs {
 
 // Code-generation choices (HS_JIT_OPTS="regs=20,win=48,avail=reg,dur=sel")
 struct JitOpts {
-    int reg_budget = 20;   // end times kept in registers at once
-    int reg_window = 48;   // ... when consumed within this many positions
-    bool avail_smem = false;  // per-device available times in shared memory
-    bool dur_smem = false;    // latency table in shared memory (else selects)
+    // defaults from the B200 A/B sweep (profiles/README.md, r1c)
+    int reg_budget = 64;   // end times kept in registers at once
+    int reg_window = 400;  // ... when consumed within this many positions
+    bool avail_smem = true;   // per-device available times in shared memory
+    bool dur_smem = true;     // latency table in shared memory (else selects)
     static JitOpts from_env();
 };
 

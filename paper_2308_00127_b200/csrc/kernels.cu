@@ -282,6 +282,56 @@ __global__ void reach_kernel(const uint8_t *blob, DevLayout lay, int NT, int wor
     }
 }
 
+// K7: Newman modularity of many partitions of the undirected shadow, one
+// CTA per partition: integer intra-edge counts and degree sums per
+// community by shared-memory atomics (exact), then the same binary64
+// sequence as networkx.community.modularity: per community
+// L_c / m - ((res * d_c) * d_c) * norm, summed in community order.
+__global__ void modularity_kernel(const uint8_t *blob, DevLayout lay, int NT,
+                                  const int32_t *labels, int ncomm, double res,
+                                  double m, double norm, double *out,
+                                  uint8_t *status) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    unsigned long long *Lc = reinterpret_cast<unsigned long long *>(sm);
+    unsigned long long *Dc = Lc + ncomm;
+    __shared__ int bad;
+    const int32_t *so = reinterpret_cast<const int32_t *>(blob + lay.rc_succ_off);
+    const int32_t *sv = reinterpret_cast<const int32_t *>(blob + lay.rc_succ);
+    const int32_t *lab = labels + (int64_t)blockIdx.x * NT;
+    for (int c = threadIdx.x; c < ncomm; c += blockDim.x) Lc[c] = Dc[c] = 0ull;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < NT; t += blockDim.x) {
+        const int a = lab[t];
+        if (a < 0 || a >= ncomm) {
+            bad = 1;
+            continue;
+        }
+        const unsigned long long deg =
+            (unsigned long long)(so[t + 1] - so[t]);  // out-degree
+        atomicAdd(&Dc[a], deg);
+        for (int e = so[t]; e < so[t + 1]; ++e) {
+            const int b = lab[sv[e]];
+            if (b >= 0 && b < ncomm) {
+                atomicAdd(&Dc[b], 1ull);  // in-degree of the successor
+                if (b == a) atomicAdd(&Lc[a], 1ull);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double q = 0.0;
+        for (int c = 0; c < ncomm; ++c) {
+            const double contrib = __ddiv_rn((double)Lc[c], m) -
+                                   __dmul_rn(__dmul_rn(__dmul_rn(res, (double)Dc[c]),
+                                                       (double)Dc[c]), norm);
+            q = q + contrib;
+        }
+        out[blockIdx.x] = q;
+        if (status) status[blockIdx.x] = (uint8_t)bad;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -343,6 +393,26 @@ int launch_cp(const uint8_t *blob, const DevLayout &lay, int V, int words,
                                                 out, status, scratch);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HS_OK : cuda_fail(e, err, "cp launch");
+}
+
+int launch_modularity(const uint8_t *blob, const DevLayout &lay, int NT,
+                      const int32_t *labels, int64_t P, int ncomm, double res,
+                      double m, double norm, double *out, uint8_t *status,
+                      cudaStream_t stream, std::string *err) {
+    const size_t smem = size_t(ncomm) * 16;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(
+            modularity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return cuda_fail(e, err, "modularity smem");
+    }
+    for (int64_t lo = 0; lo < P; lo += 65535) {
+        const int64_t nb = P - lo < 65535 ? P - lo : 65535;
+        modularity_kernel<<<(unsigned)nb, 256, smem, stream>>>(
+            blob, lay, NT, labels + lo * NT, ncomm, res, m, norm, out + lo,
+            status ? status + lo : nullptr);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HS_OK : cuda_fail(e, err, "modularity launch");
 }
 
 int launch_reach(const uint8_t *blob, const DevLayout &lay, int NT, int words,

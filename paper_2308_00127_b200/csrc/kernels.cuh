@@ -23,6 +23,10 @@ int launch_eval(const DevState &ds, bool cls, const EvalParams &p, int grid,
 int launch_cp(const uint8_t *blob, const DevLayout &lay, int V, int words,
               const uint64_t *masks, int64_t nsub, double *out, uint8_t *status,
               double *scratch, cudaStream_t stream, std::string *err);
+int launch_modularity(const uint8_t *blob, const DevLayout &lay, int NT,
+                      const int32_t *labels, int64_t P, int ncomm, double res,
+                      double m, double norm, double *out, uint8_t *status,
+                      cudaStream_t stream, std::string *err);
 int launch_reach(const uint8_t *blob, const DevLayout &lay, int NT, int words,
                  uint64_t *desc, uint64_t *anc, cudaStream_t stream,
                  std::string *err);

@@ -16,7 +16,8 @@ from paper_2308_00127_b200.plan import get_plan  # noqa: E402
 from oracle import hs_oracle as O  # noqa: E402
 from oracle.hs_oracle_c import CTables  # noqa: E402
 
-ELIGIBLE = [n for n in INSTANCES if n not in ("tf96",)]
+ELIGIBLE = [n for n in INSTANCES
+            if n not in ("tf96", "ws1000", "ws_stack_10x100")]
 
 
 def _hexes(ms, st):

@@ -38,5 +38,7 @@ def test_scope():
     with pytest.raises(hs.GraphError):
         p.specialized_source()
     assert Plan(*hs.load_instance(instance_doc("ws200")), 1).jit_eligible()
+    # straight-line code for ~1000 tasks would take ptxas minutes
+    assert not Plan(*hs.load_instance(instance_doc("ws1000")), 1).jit_eligible()
     for doc in random_docs()[:50]:  # per-pair bandwidths: out of scope
         assert not Plan(*hs.load_instance(doc), doc["L"]).jit_eligible()

@@ -87,3 +87,28 @@ def test_argmin_first_semantics():
     assert O.argmin_first(v) == (1.0, 2)
     assert O.argmin_first(np.full(4, np.inf)) == (np.inf, 0)
     assert O.argmin_first(np.array([])) == (np.inf, -1)
+
+
+def test_search_oracle_golden():
+    """The CPU SA / EA restatement (oracle/hs_search.py) reproduces the
+    reference's recorded runs (objective + mapping)."""
+    from oracle import hs_search as S
+    checked = 0
+    for e in golden("heuristics"):
+        inst = O.Instance.from_doc(e)
+        tb = O.build_tables(inst, e["L"])
+        for run in e["search"]:
+            if "error" in run or run["budget"] > 50:
+                continue
+            if run["algo"] == "sa":
+                fit, genes = S.simulated_annealing(inst, e["L"], run["seed"],
+                                                   run["budget"])
+            else:
+                fit, genes = S.one_plus_one_ea(inst, e["L"], run["seed"],
+                                               run["budget"],
+                                               biased=run["algo"] == "ea")
+            assert fhex(fit) == run["objective"]
+            assert {t: tb.devs[k] for t, k in zip(tb.order, genes)} == \
+                run["mapping"]
+            checked += 1
+    assert checked > 50
