@@ -404,6 +404,68 @@ int hs_trace(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
                     static_cast<cudaStream_t>(stream));
 }
 
+namespace {
+
+// Per-thread staging for small host batches (search-loop windows): one
+// pinned host buffer and one device buffer reused across calls, so a call
+// is one H2D, one launch, one D2H and one stream sync.
+struct SmallWs {
+    int dev = -1;
+    uint8_t *d = nullptr, *h = nullptr;
+    size_t cap = 0;
+    ~SmallWs() {
+        if (d) cudaFree(d);
+        if (h) cudaFreeHost(h);
+    }
+};
+thread_local SmallWs g_small;
+constexpr int64_t kSmallN = 1 << 16;
+
+int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
+                    int64_t ld, double *h_makespan, uint8_t *h_status,
+                    hs_best *h_best, int64_t index_base, cudaStream_t s) {
+    const int64_t V = plan->p.V;
+    const int64_t lds = plan->p.pref_ld();  // compact, TMA-friendly stride
+    const size_t gb = (size_t(n * lds) + 255) & ~size_t(255);
+    const size_t need = gb + size_t(n) * 9 + 64;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    SmallWs &w = g_small;
+    if (w.dev != dev || w.cap < need) {
+        if (w.d) cudaFree(w.d);
+        if (w.h) cudaFreeHost(w.h);
+        w.d = w.h = nullptr;
+        const size_t cap = std::max(need, size_t(1) << 20);
+        CK(cudaMalloc(&w.d, cap));
+        CK(cudaMallocHost(&w.h, cap));
+        w.cap = cap;
+        w.dev = dev;
+    }
+    for (int64_t r = 0; r < n; ++r)
+        std::memcpy(w.h + r * lds, h_genes + r * ld, size_t(V));
+    double *dm = reinterpret_cast<double *>(w.d + gb);
+    uint8_t *dst = w.d + gb + size_t(n) * 8;
+    hs_best *db = reinterpret_cast<hs_best *>(w.d + ((gb + size_t(n) * 9 + 15) & ~size_t(15)));
+    CK(cudaMemcpyAsync(w.d, w.h, size_t(n * lds), cudaMemcpyHostToDevice, s));
+    int rc = run_eval(plan, w.d, n, lds, 0, 0, 0, nullptr, nullptr, 0, dm, dst,
+                      nullptr, nullptr, h_best ? db : nullptr, index_base, s);
+    if (rc) return rc;
+    // results come back contiguously: makespans, statuses, best
+    const size_t back = (reinterpret_cast<uint8_t *>(db) - reinterpret_cast<uint8_t *>(dm)) +
+                        (h_best ? sizeof(hs_best) : 0);
+    CK(cudaMemcpyAsync(w.h, dm, back, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h_makespan) std::memcpy(h_makespan, w.h, size_t(n) * 8);
+    if (h_status) std::memcpy(h_status, w.h + size_t(n) * 8, size_t(n));
+    if (h_best)
+        std::memcpy(h_best, w.h + (reinterpret_cast<uint8_t *>(db) -
+                                   reinterpret_cast<uint8_t *>(dm)),
+                    sizeof(hs_best));
+    return HS_OK;
+}
+
+}  // namespace
+
 int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
                  int64_t ld, double *h_makespan, uint8_t *h_status,
                  hs_best *h_best, int64_t index_base, void *stream) {
@@ -411,6 +473,9 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     if (n < 0 || (n > 0 && (!h_genes || ld < plan->p.V)))
         return set_err(HS_EINVAL, "genes must be [n x ld] with ld >= V");
     cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    if (n > 0 && n <= kSmallN && plan->p.V > 0)
+        return eval_host_small(plan, h_genes, n, ld, h_makespan, h_status, h_best,
+                               index_base, s0);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 1 << 19));
     const int64_t nchunks = n > 0 ? (n + chunk - 1) / chunk : 1;
     const size_t gbytes = size_t(chunk * ld);

@@ -192,8 +192,12 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int i = 0; i < V; ++i) {
             const std::string di = "d" + std::to_string(i);
             s += "    // " + p.task_ids[p.order[i]] + "\n";
-            std::snprintf(buf, sizeof buf, "    const int %s = g[%d]; gmax = max(gmax, %s);\n",
-                          di.c_str(), i, di.c_str());
+            // raw gene for the range check; clamped for table / state
+            // indexing (lanes past the last row read stale tile bytes)
+            std::snprintf(buf, sizeof buf,
+                          "    const int g%d = g[%d]; gmax = max(gmax, g%d);\n"
+                          "    const int %s = min(g%d, %d);\n",
+                          i, i, i, di.c_str(), i, K - 1);
             s += buf;
             // arrivals of the predecessors (ready_time, :67-78)
             std::vector<std::string> xs;

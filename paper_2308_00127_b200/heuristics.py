@@ -88,9 +88,17 @@ def _device_buffers(n: int, ld: int, V: int, trace: bool):
 
 def _eval_rows(plan: Plan, rows: np.ndarray, trace: bool = False):
     """Evaluate uint8 rows [n, V] on the GPU -> (makespan, status[, starts])
-    as numpy arrays."""
-    import torch
+    as numpy arrays. Without a trace this is one hs_eval_host call (pinned
+    per-thread staging, one H2D / launch / D2H)."""
     n, V = rows.shape
+    if not trace:
+        rows = np.ascontiguousarray(rows, np.uint8)
+        ms = np.empty(n, np.float64)
+        st = np.empty(n, np.uint8)
+        if n:
+            plan.eval_host(rows, ms, st, None)
+        return ms, st
+    import torch
     ld = plan.pref_ld if V else 1
     c = _device_buffers(n, ld, V, trace)
     host = np.zeros((n, ld), np.uint8)
@@ -99,14 +107,10 @@ def _eval_rows(plan: Plan, rows: np.ndarray, trace: bool = False):
         g = c.genes[: n * ld].view(n, ld)
         g.copy_(torch.from_numpy(host), non_blocking=False)
         ms, st = c.ms[:n], c.st[:n]
-        if trace:
-            sv = c.starts[: n * V].view(n, V) if V else c.starts[:0]
-            plan.trace(g, c.starts, ms, st, stream=c.stream)
-            out = (ms.cpu().numpy(), st.cpu().numpy(),
-                   sv.cpu().numpy().reshape(n, V))
-        else:
-            plan.eval(g, ms, st, None, stream=c.stream)
-            out = (ms.cpu().numpy(), st.cpu().numpy())
+        sv = c.starts[: n * V].view(n, V) if V else c.starts[:0]
+        plan.trace(g, c.starts, ms, st, stream=c.stream)
+        out = (ms.cpu().numpy(), st.cpu().numpy(),
+               sv.cpu().numpy().reshape(n, V))
     return out
 
 
@@ -525,19 +529,18 @@ def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
     step = 0
     while step < budget:
         k = min(window, budget - step)
-        S, st = R.peek(gen, k * (V + 2) + 64)
-        muts = []
+        S, words, st = R.peek_words(gen, k * (V + 2) + 64)
         try:
-            for _ in range(k):
-                m = []
-                for pos in range(V):
-                    u, st = S.random(st)
-                    if u < p:
-                        val, st = S.integers(st, n_dev)
-                        m.append((pos, val))
-                muts.append((m, st))
+            muts = R.ea_mutations(S, words, st, k, V, n_dev, p)
         except IndexError:
-            pass
+            muts = []
+            for kk in (k // 2, k // 4, 1):
+                try:
+                    muts = R.ea_mutations(S, words, st, max(kk, 1), V, n_dev,
+                                          p)
+                    break
+                except IndexError:
+                    continue
         if not muts:
             raise RuntimeError("RNG peek window too small")
         j = 0

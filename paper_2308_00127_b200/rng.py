@@ -85,3 +85,48 @@ def commit(rng: np.random.Generator, state) -> None:
     st["has_uint32"] = int(has)
     st["uinteger"] = int(u)
     bg.state = st
+
+
+def ea_mutations(S: RawStream, words: np.ndarray, st, steps: int, V: int,
+                 n_dev: int, p: float):
+    """Mutation lists of `steps` (1+1) EA steps (heuristics.py:321-325: for
+    each position, ``random() < p`` then ``integers(n_dev)``), vectorised
+    over the runs of misses: random() draws are whole words and leave the
+    32-bit buffer alone, so only the hits need the sequential model.
+    Returns [(mutations, state after the step)]; raises IndexError when the
+    peeked words run out (the caller shortens its window)."""
+    W = len(words)
+    u = (words >> np.uint64(11)).astype(np.float64) * _D53
+    idx = np.where(u < p, np.arange(W), W)
+    nxt = np.minimum.accumulate(idx[::-1])[::-1].tolist()
+    out = []
+    i, has, c = st
+    for _ in range(steps):
+        pos = 0
+        muts = []
+        while pos < V:
+            rem = V - pos
+            if i + rem > W:
+                raise IndexError("peek window exhausted")
+            j = nxt[i]
+            if j >= i + rem:
+                i += rem
+                break
+            pos += j - i
+            i = j + 1
+            val, (i, has, c) = S.integers((i, has, c), n_dev)
+            muts.append((pos, val))
+            pos += 1
+        out.append((muts, (i, has, c)))
+    return out
+
+
+def peek_words(rng: np.random.Generator, nwords: int):
+    """Like peek() but also returns the raw words as a numpy array."""
+    bg = rng.bit_generator
+    st = bg.state
+    clone = type(bg)()
+    clone.state = st
+    words = clone.random_raw(nwords)
+    return (RawStream(words), words,
+            (0, int(st["has_uint32"]), int(st["uinteger"])))

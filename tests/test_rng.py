@@ -1,0 +1,55 @@
+"""rng.py replays numpy's PCG64 Generator exactly (the basis of the exact
+speculative SA / EA batches)."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+
+from paper_2308_00127_b200 import rng as R
+
+
+def test_stream_model_matches_numpy():
+    for seed in range(60):
+        real = np.random.default_rng(seed)
+        mirror = np.random.default_rng(seed)
+        pr = random.Random(seed)
+        for _ in range(20):
+            S, st = R.peek(mirror, 200)
+            for _ in range(pr.randint(1, 12)):
+                if pr.random() < 0.4:
+                    a = real.random()
+                    b, st = S.random(st)
+                else:
+                    h = pr.choice([1, 2, 3, 5, 7, 30, 200, 1000, 2**31 + 11,
+                                   2**32])
+                    a = int(real.integers(h))
+                    b, st = S.integers(st, h)
+                assert a == b
+            R.commit(mirror, st)
+        s1, s2 = real.bit_generator.state, mirror.bit_generator.state
+        assert s1["state"] == s2["state"]
+        assert s1["has_uint32"] == s2["has_uint32"]
+        if s1["has_uint32"]:
+            assert s1["uinteger"] == s2["uinteger"]
+
+
+def test_ea_mutations_match_reference_loop():
+    for seed, V, n_dev in [(0, 32, 3), (1, 202, 3), (2, 17, 2), (3, 50, 4),
+                           (4, 5, 1)]:
+        p = 1.0 / V
+        real = np.random.default_rng(seed)
+        mirror = np.random.default_rng(seed)
+        for _ in range(5):
+            steps = 40
+            S, words, st = R.peek_words(mirror, steps * (V + 2) + 64)
+            got = R.ea_mutations(S, words, st, steps, V, n_dev, p)
+            for muts, _ in got:
+                want = []
+                for pos in range(V):  # heuristics.py:323-325
+                    if real.random() < p:
+                        want.append((pos, int(real.integers(n_dev))))
+                assert muts == want
+            R.commit(mirror, got[-1][1])
+        assert real.bit_generator.state["state"] == \
+            mirror.bit_generator.state["state"]
