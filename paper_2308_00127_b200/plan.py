@@ -197,7 +197,8 @@ class Plan:
         genes = np.ascontiguousarray(genes, dtype=np.uint8) \
             if genes.strides[-1] != 1 else genes
         n = genes.shape[0]
-        ld = genes.strides[0] if n else self.V
+        # a length-1 leading axis may carry stride 0 (x[None, :])
+        ld = genes.strides[0] if n > 1 else max(genes.shape[1], self.V)
         N.check(self._lib.hs_eval_host(
             self.handle, genes.ctypes.data if n else None, n, ld,
             makespan.ctypes.data if makespan is not None else None,
