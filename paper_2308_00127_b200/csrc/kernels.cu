@@ -286,7 +286,8 @@ __global__ void reach_kernel(const uint8_t *blob, DevLayout lay, int NT, int wor
 // CTA per partition: integer intra-edge counts and degree sums per
 // community by shared-memory atomics (exact), then the same binary64
 // sequence as networkx.community.modularity: per community
-// L_c / m - ((res * d_c) * d_c) * norm, summed in community order.
+// L_c / m - ((res * d_c) * d_c) * norm, summed in community order by
+// CPython's compensated float sum().
 __global__ void modularity_kernel(const uint8_t *blob, DevLayout lay, int NT,
                                   const int32_t *labels, int ncomm, double res,
                                   double m, double norm, double *out,
@@ -320,14 +321,22 @@ __global__ void modularity_kernel(const uint8_t *blob, DevLayout lay, int NT,
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double q = 0.0;
+        // Python >= 3.12 sum() over floats: Neumaier-compensated, with the
+        // compensation added once at the end when finite and nonzero
+        double f = 0.0, comp = 0.0;
         for (int c = 0; c < ncomm; ++c) {
-            const double contrib = __ddiv_rn((double)Lc[c], m) -
-                                   __dmul_rn(__dmul_rn(__dmul_rn(res, (double)Dc[c]),
-                                                       (double)Dc[c]), norm);
-            q = q + contrib;
+            const double x = __ddiv_rn((double)Lc[c], m) -
+                             __dmul_rn(__dmul_rn(__dmul_rn(res, (double)Dc[c]),
+                                                 (double)Dc[c]), norm);
+            const double t = f + x;
+            if (fabs(f) >= fabs(x))
+                comp += (f - t) + x;
+            else
+                comp += (x - t) + f;
+            f = t;
         }
-        out[blockIdx.x] = q;
+        if (comp != 0.0 && isfinite(comp)) f += comp;
+        out[blockIdx.x] = f;
         if (status) status[blockIdx.x] = (uint8_t)bad;
     }
 }
