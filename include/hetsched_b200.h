@@ -97,6 +97,8 @@ typedef struct hs_plan_info {
     int32_t pref_ld;              /* genome row stride that makes the staged
                                      tile bank-conflict free (>= V) */
     int32_t specializable;        /* hs_plan_specialize can serve this plan */
+    int32_t batched_options;      /* batched-variant plans: options (genes) */
+    int32_t max_parts;            /* batched-variant plans: parts per task */
 } hs_plan_info;
 
 typedef struct hs_best {
@@ -110,6 +112,18 @@ int hs_abi_version(void);
 
 int hs_plan_create(const hs_instance_desc *desc, hs_plan **out);
 void hs_plan_destroy(hs_plan *plan);
+/* Batched-variant plan (heuristics.py:337-433, bMET / bGreedy placement):
+ * the genome holds one OPTION index per position, an option being a
+ * decomposition of the L inputs into allowed sub-batch sizes (`splits`, or
+ * L/4, L/2, 3L/4, L where integral) on distinct devices, enumerated in
+ * batched_variant's order. hs_eval* / hs_trace then evaluate extended
+ * genomes (hs_trace writes starts [n x V x max_parts]). */
+int hs_plan_create_batched(const hs_instance_desc *desc, const int32_t *splits,
+                           int32_t n_splits, hs_plan **out);
+/* Option table: [n_opt][max_parts][4] = sorted-device index, first input,
+ * last input (1-based), size; unused parts are -1. */
+int hs_plan_batched_options(const hs_plan *plan, int32_t *n_opt,
+                            int32_t *max_parts, int32_t *table);
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
 /* Specialise the evaluator to this plan on the current device: the plan is
  * emitted as straight-line CUDA and compiled by NVRTC for sm_100a (one-time

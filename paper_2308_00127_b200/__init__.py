@@ -21,6 +21,8 @@ from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
                      dep_subgraph, lower_bound, pre_subgraph)
 from .splitting import ModuleSolver, gpu_module_solver
+from .batched import (batched_genes_from_schedule, batched_options,
+                      decode_batched, fitness_batched, random_search_batched)
 from .modularity import (decomposition_modularity, modularity,
                          modularity_batch)
 

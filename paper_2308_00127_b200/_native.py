@@ -49,7 +49,7 @@ class PlanInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "V", "E", "K", "L", "live_slots", "n_classes", "uniform_comm",
         "full_mesh", "mem_check", "all_batch_ok", "latency_complete", "words",
-        "pref_ld", "specializable")]
+        "pref_ld", "specializable", "batched_options", "max_parts")]
 
 
 class Best(C.Structure):
@@ -80,6 +80,9 @@ def load() -> C.CDLL:
             "hs_abi_version": (C.c_int, []),
             "hs_plan_create": (C.c_int, [_p(InstanceDesc), _p(vp)]),
             "hs_plan_destroy": (None, [vp]),
+            "hs_plan_create_batched": (C.c_int, [_p(InstanceDesc), vp, i32,
+                                                 _p(vp)]),
+            "hs_plan_batched_options": (C.c_int, [vp, vp, vp, vp]),
             "hs_plan_get_info": (C.c_int, [vp, _p(PlanInfo)]),
             "hs_plan_order": (C.c_int, [vp, vp, vp]),
             "hs_plan_specialize": (C.c_int, [vp, _p(C.c_double)]),
@@ -111,7 +114,8 @@ def load() -> C.CDLL:
 def exported_symbols() -> list[str]:
     """Names declared by include/hetsched_b200.h (checked by the tests)."""
     return ["hs_last_error", "hs_abi_version", "hs_plan_create",
-            "hs_plan_destroy", "hs_plan_get_info", "hs_plan_order",
+            "hs_plan_destroy", "hs_plan_create_batched",
+            "hs_plan_batched_options", "hs_plan_get_info", "hs_plan_order",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
             "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge"]

@@ -104,7 +104,9 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
     ds->kt = kt_of(p.K);
     ds->ld_cap = p.pref_ld() + 16;
     const bool cls = !p.uniform_comm;
-    const int64_t per_lane = ds->ld_cap + int64_t(p.live_slots) * 8 +
+    if (p.batched) ds->kt = 0;  // device state in shared memory
+    const int64_t slot_bytes = int64_t(p.live_slots) * 8 * (p.batched ? p.P : 1);
+    const int64_t per_lane = ds->ld_cap + slot_bytes +
                              (ds->kt == 0 ? int64_t(16) * p.K : 0);
     const int64_t budget = int64_t(optin) - 16 - 1024;
     auto lanes_for = [&](int64_t plan_bytes) {
@@ -121,12 +123,13 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
         ds->smem_tile = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0);
         ds->smem_ends = ds->smem_tile +
                         ((int64_t(ds->T) * ds->ld_cap + 15) & ~int64_t(15));
-        ds->smem_kstate = ds->smem_ends + int64_t(p.live_slots) * ds->T * 8;
+        ds->smem_kstate = ds->smem_ends + slot_bytes * ds->T;
         ds->smem = ds->smem_kstate +
                    (ds->kt == 0 ? int64_t(2) * p.K * ds->T * 8 : 0);
         int blocks = 0;
-        if (eval_occupancy(ds->kt, cls, ds->T, ds->smem, &blocks) != HS_OK)
-            blocks = 0;
+        const int orc = p.batched ? beval_occupancy(ds->T, ds->smem, &blocks)
+                                  : eval_occupancy(ds->kt, cls, ds->T, ds->smem, &blocks);
+        if (orc != HS_OK) blocks = 0;
         ds->blocks_per_sm = blocks;
     }
     if (ds->blocks_per_sm < 1) {  // eval unusable; bounds kernels still run
@@ -137,9 +140,11 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
     std::vector<uint8_t> img = p.blob;
     NodeRec *nodes = reinterpret_cast<NodeRec *>(img.data() + p.lay.node);
     EdgeRec *edges = reinterpret_cast<EdgeRec *>(img.data() + p.lay.edge);
-    for (int i = 0; i < p.V; ++i)
-        if (nodes[i].out_slot >= 0) nodes[i].out_slot *= ds->lanes;
-    for (size_t q = 0; q < p.edges.size(); ++q) edges[q].slot *= ds->lanes;
+    if (!p.batched) {  // batched: the kernel scales (slot * P + part) itself
+        for (int i = 0; i < p.V; ++i)
+            if (nodes[i].out_slot >= 0) nodes[i].out_slot *= ds->lanes;
+        for (size_t q = 0; q < p.edges.size(); ++q) edges[q].slot *= ds->lanes;
+    }
     cudaGetLastError();  // clear a sticky-free error from the occupancy probe
     e = cudaMalloc(&ds->blob, img.size());
     if (e == cudaSuccess)
@@ -200,7 +205,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
         genes = static_cast<const uint8_t *>(repack.ptr);
         ld = pl;
     }
-    const hs::JitModule *jm = hs::find_jit(p, ds->device);
+    const hs::JitModule *jm = p.batched ? nullptr : hs::find_jit(p, ds->device);
     const int lanes = jm ? jm->lanes : ds->lanes;
     const int64_t ntiles = (n + lanes - 1) / lanes;
     const int64_t cap = jm ? int64_t(jm->sms) * jm->blocks_per_sm
@@ -222,6 +227,10 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.eval_bytes = p.lay.eval_bytes;
     a.V = p.V;
     a.K = p.K;
+    a.gene_range = p.batched ? p.n_opt : p.K;
+    a.n_opt = p.n_opt;
+    a.P = p.P;
+    a.n_cls = p.n_cls;
     a.flags = flags_of(p);
     a.plan_smem = ds->plan_smem ? 1 : 0;
     a.lanes = lanes;
@@ -249,6 +258,8 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     if (jm) {
         a.slots = jm->slots;
         rc = hs::jit_launch(*jm, a, grid, stream, &err);
+    } else if (p.batched) {
+        rc = hs::launch_beval(*ds, a, grid, stream, &err);
     } else {
         rc = hs::launch_eval(*ds, !p.uniform_comm, a, grid, stream, &err);
     }
@@ -279,6 +290,35 @@ int hs_plan_create(const hs_instance_desc *desc, hs_plan **out) {
 }
 
 void hs_plan_destroy(hs_plan *plan) { delete plan; }
+
+int hs_plan_create_batched(const hs_instance_desc *desc, const int32_t *splits,
+                           int32_t n_splits, hs_plan **out) {
+    if (!desc || !out) return set_err(HS_EINVAL, "null argument");
+    hs_plan *pl = new (std::nothrow) hs_plan();
+    if (!pl) return set_err(HS_ENOMEM, "out of host memory");
+    std::string err;
+    hs::BatchedSpec bs;
+    bs.splits = splits;
+    bs.n_splits = n_splits;
+    int rc = hs::build_plan(*desc, pl->p, &err, &bs);
+    if (rc) {
+        delete pl;
+        return set_err(rc, err);
+    }
+    *out = pl;
+    return HS_OK;
+}
+
+int hs_plan_batched_options(const hs_plan *plan, int32_t *n_opt, int32_t *max_parts,
+                            int32_t *table) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    const hs::Plan &p = plan->p;
+    if (!p.batched) return set_err(HS_EINVAL, "not a batched-variant plan");
+    if (n_opt) *n_opt = p.n_opt;
+    if (max_parts) *max_parts = p.P;
+    if (table) std::copy(p.opt_tab.begin(), p.opt_tab.end(), table);
+    return HS_OK;
+}
 
 int hs_plan_specialize(const hs_plan *plan, double *compile_ms) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
@@ -346,6 +386,8 @@ int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info) {
     info->words = p.words;
     info->pref_ld = p.pref_ld();
     info->specializable = hs::jit_eligible(p) ? 1 : 0;
+    info->batched_options = p.batched ? p.n_opt : 0;
+    info->max_parts = p.batched ? p.P : 1;
     return HS_OK;
 }
 

@@ -20,6 +20,9 @@ struct DevLayout {
     hs_i64 rc_succ_off, rc_succ, rc_pred_off, rc_pred, rc_order;
     hs_i64 total;
     hs_i64 eval_bytes;  // [0, eval_bytes) = evaluator tables, 16-aligned
+    // batched-variant plans: option table [n_opt][P] of {dev, lo, hi, size}
+    // (int32 x4), parts per option [n_opt], durations [V][n_opt][P] + flags
+    hs_i64 bopt, bnp, bdur, bdur_ok;
 };
 
 // One predecessor relaxation: `slot` = the predecessor's end-time slot
@@ -64,6 +67,9 @@ struct EvalParams {
     DevLayout lay;
     hs_i64 eval_bytes;
     int V, K;
+    int gene_range;     // genes are in [0, gene_range): K, or n_opt (batched)
+    int n_opt, P;       // batched-variant plans
+    int n_cls;
     hs_u32 flags;
     int plan_smem;
     int lanes, ld_s, slots;
@@ -220,7 +226,7 @@ static __device__ __noinline__ void reduce_best(double bc, hs_i64 bi, Best *part
 // K6: on-device candidate rows (oracle/hs_oracle.py::gen_genes, or
 // mixed-radix enumeration), expanded over the group map.
 __device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 cidx) {
-    const int NG = a.n_groups, K = a.K, V = a.V;
+    const int NG = a.n_groups, K = a.gene_range, V = a.V;
     const hs_u64 c = (hs_u64)cidx;
     if (a.gen == 1) {
         const int W4 = (NG + 3) >> 2;

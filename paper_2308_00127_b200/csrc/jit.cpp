@@ -127,7 +127,7 @@ static int64_t dur_bytes(const Plan &p) {
 constexpr int kJitMaxV = 512, kJitMaxE = 2048;
 
 bool jit_eligible(const Plan &p) {
-    return p.K <= 4 && p.uniform_comm && !p.mem_check && p.all_batch_ok &&
+    return !p.batched && p.K <= 4 && p.uniform_comm && !p.mem_check && p.all_batch_ok &&
            p.latency_complete && !p.nan_possible && p.V > 0 &&
            p.V <= kJitMaxV && p.E <= kJitMaxE;
 }

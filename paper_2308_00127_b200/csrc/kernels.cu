@@ -168,7 +168,116 @@ struct PlanBody {
     }
 };
 
+// Batched-variant extended genome (heuristics.py:363-433, non-insertion):
+// gene = option (decomposition of L x distinct devices); per part, ready
+// time over the predecessors' parts holding the part's inputs, start at
+// max(ready, last end on the device). Like batched_variant, no memory or
+// batch-size check (options are pre-filtered to supported sizes).
+struct BatchedBody {
+    const NodeRec *nodes;
+    const EdgeRec *edges;
+    const int *bopt;     // [n_opt][P][4] = dev, lo, hi, size
+    const int *bnp;      // [n_opt]
+    const double *bdur;  // [V][n_opt][P]
+    const hs_u8 *bdur_ok;
+    const double *ctab;
+    const hs_u16 *bclass;
+    double *ends;        // [slot * P + part][lanes]
+    double *kstate;      // [K][lanes] device-available times
+    double *starts;      // [n][V][P]
+    int lanes, V, K, n_opt, P, ncls;
+    bool nan;
+
+    __device__ __forceinline__ void run(const hs_u8 *grow, int li, hs_i64 cand,
+                                        bool valid, double &ms_out, int &st_out) {
+        double *ecol = ends + li;
+        double *av = kstate + li;
+        for (int k = 0; k < K; ++k) av[k * lanes] = 0.0;
+        double ms = 0.0;
+        int st = 0, bad = 0;
+        for (int i = 0; i < V; ++i) {
+            const NodeRec nr = nodes[i];
+            int o = grow[i];
+            bad |= o >= n_opt;
+            o = o < n_opt ? o : 0;
+            const int np = bnp[o];
+            for (int k = 0; k < np; ++k) {
+                const int *q = bopt + (o * P + k) * 4;
+                const int d = q[0], lo = q[1], hi = q[2];
+                double r = 0.0;
+                int nolink = 0;
+                for (int e = nr.e_begin; e < nr.e_end; ++e) {
+                    const EdgeRec er = edges[e];
+                    int op = grow[er.gpos];
+                    op = op < n_opt ? op : 0;
+                    const int npp = bnp[op];
+                    // the predecessor's parts holding inputs lo..hi, in
+                    // input order (Python iterates l = lo..hi)
+                    for (int m = 0; m < npp; ++m) {
+                        const int *qq = bopt + (op * P + m) * 4;
+                        if (qq[2] < lo || qq[1] > hi) continue;
+                        int cls = bclass[qq[0] * K + d];
+                        if (cls == 0xFFFF) {
+                            nolink = 1;
+                            cls = 0;
+                        }
+                        const double x = ecol[(er.slot * P + m) * lanes] + ctab[er.crow + cls];
+                        r = pymax(r, x);
+                    }
+                }
+                if (nolink && !st) st = ST_LINK;
+                const hs_i64 at = ((hs_i64)i * n_opt + o) * P + k;
+                if (!bdur_ok[at] && !st) st = ST_MISSING;
+                const double s = pymax(r, av[d * lanes]);
+                const double e = s + bdur[at];
+                if (starts && valid) starts[(cand * V + i) * P + k] = s;
+                if (nr.out_slot >= 0) ecol[(nr.out_slot * P + k) * lanes] = e;
+                av[d * lanes] = e;
+                ms = pymax(ms, e);
+            }
+        }
+        if (bad) st = ST_GENE;
+        if (st) ms = st >= ST_MISSING ? knan() : kinf();
+        ms_out = ms;
+        st_out = st;
+    }
+};
+
 }  // namespace
+
+// Batched-variant evaluator (one lane per extended genome).
+__global__ void __launch_bounds__(512) beval_kernel(const EvalParams a) {
+    extern __shared__ __align__(16) hs_u8 smem[];
+    const hs_u8 *plan = a.blob;
+    if (a.plan_smem) {
+        hs_u8 *sp = smem + 16;
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.blob);
+        uint4 *dst = reinterpret_cast<uint4 *>(sp);
+        for (hs_i64 q = threadIdx.x; q < a.eval_bytes / 16; q += blockDim.x)
+            dst[q] = src[q];
+        plan = sp;
+    }
+    BatchedBody body;
+    body.nodes = reinterpret_cast<const NodeRec *>(plan + a.lay.node);
+    body.edges = reinterpret_cast<const EdgeRec *>(plan + a.lay.edge);
+    body.bopt = reinterpret_cast<const int *>(plan + a.lay.bopt);
+    body.bnp = reinterpret_cast<const int *>(plan + a.lay.bnp);
+    body.bdur = reinterpret_cast<const double *>(plan + a.lay.bdur);
+    body.bdur_ok = plan + a.lay.bdur_ok;
+    body.ctab = reinterpret_cast<const double *>(plan + a.lay.ctab);
+    body.bclass = reinterpret_cast<const hs_u16 *>(plan + a.lay.bclass);
+    body.ends = reinterpret_cast<double *>(smem + a.smem_ends);
+    body.kstate = reinterpret_cast<double *>(smem + a.smem_kstate);
+    body.starts = a.starts;
+    body.lanes = a.lanes;
+    body.V = a.V;
+    body.K = a.K;
+    body.n_opt = a.n_opt;
+    body.P = a.P;
+    body.ncls = a.n_cls;
+    body.nan = (a.flags & F_NAN) != 0;
+    eval_tiles(a, smem, body);
+}
 
 // K1: one lane per candidate; every lane walks the same record sequence
 // (broadcast reads), only gene-indexed lookups diverge.
@@ -362,6 +471,28 @@ static void *pick_eval(int kt, bool cls, bool fast) {
         case 4: return cls ? eval_fn<4, true>(fast) : eval_fn<4, false>(fast);
         default: return cls ? eval_fn<0, true>(fast) : eval_fn<0, false>(fast);
     }
+}
+
+int beval_occupancy(int T, size_t smem, int *blocks) {
+    if (cudaFuncSetAttribute(beval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HS_ECUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, beval_kernel, T, smem) !=
+        cudaSuccess)
+        return HS_ECUDA;
+    return HS_OK;
+}
+
+int launch_beval(const DevState &ds, const EvalParams &p, int grid,
+                 cudaStream_t stream, std::string *err) {
+    cudaError_t e = cudaFuncSetAttribute(
+        beval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ds.smem);
+    if (e != cudaSuccess) return cuda_fail(e, err, "cudaFuncSetAttribute");
+    void *args[] = {(void *)&p};
+    e = cudaLaunchKernel((const void *)beval_kernel, dim3(grid), dim3(ds.T), args,
+                         ds.smem, stream);
+    if (e != cudaSuccess) return cuda_fail(e, err, "batched eval launch");
+    return HS_OK;
 }
 
 int eval_occupancy(int kt, bool cls, int T, size_t smem, int *blocks) {

@@ -18,6 +18,9 @@ using hsk::F_NAN;
 using hsk::F_OKL;
 
 int eval_occupancy(int kt, bool cls, int T, size_t smem, int *blocks);
+int beval_occupancy(int T, size_t smem, int *blocks);
+int launch_beval(const DevState &ds, const EvalParams &p, int grid,
+                 cudaStream_t stream, std::string *err);
 int launch_eval(const DevState &ds, bool cls, const EvalParams &p, int grid,
                 cudaStream_t stream, std::string *err);
 int launch_cp(const uint8_t *blob, const DevLayout &lay, int V, int words,

@@ -37,7 +37,8 @@ int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 }  // namespace
 
-int build_plan(const hs_instance_desc &d, Plan &p, std::string *err) {
+int build_plan(const hs_instance_desc &d, Plan &p, std::string *err,
+               const BatchedSpec *bspec) {
     if (d.n_tasks < 0 || d.n_edges < 0 || d.n_devices < 1)
         return fail(err, HS_EINVAL, "need n_tasks >= 0, n_edges >= 0, "
                                     "n_devices >= 1");
@@ -211,7 +212,9 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err) {
             bcls[size_t(u) * K + v] = 1 + int(it - betas.begin());
         }
     p.n_classes = (int)betas.size();
-    p.uniform_comm = p.full_mesh && betas.size() <= 1;
+    // batched plans always carry the class tables (the batched evaluator
+    // looks communication up by (source device, destination device))
+    p.uniform_comm = p.full_mesh && betas.size() <= 1 && !bspec;
     p.n_cls = 1 + (int)betas.size();
     if (!p.uniform_comm && p.n_cls > 65535)
         return fail(err, HS_EINVAL, "too many distinct bandwidths");
@@ -326,6 +329,120 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err) {
         p.rc_pred_off[t + 1] = (int)p.rc_pred.size();
     }
 
+    // ---- batched-variant options (heuristics.py:337-392)
+    if (bspec) {
+        p.batched = true;
+        std::vector<int> sizes;
+        if (bspec->splits && bspec->n_splits > 0) {
+            sizes.assign(bspec->splits, bspec->splits + bspec->n_splits);
+        } else {
+            for (int k = 1; k <= 4; ++k)
+                if ((d.L * k) % 4 == 0 && d.L * k / 4 >= 1) sizes.push_back(d.L * k / 4);
+        }
+        std::sort(sizes.begin(), sizes.end());
+        sizes.erase(std::unique(sizes.begin(), sizes.end()), sizes.end());
+        std::vector<std::vector<int>> decomps;
+        std::vector<int> acc;
+        std::function<void(int, int)> rec = [&](int remaining, int start) {
+            if (remaining == 0) {
+                decomps.push_back(acc);
+                return;
+            }
+            if ((int)acc.size() >= K) return;
+            for (int k = start; k < (int)sizes.size(); ++k)
+                if (sizes[k] <= remaining) {
+                    acc.push_back(sizes[k]);
+                    rec(remaining - sizes[k], k);
+                    acc.pop_back();
+                }
+        };
+        if (d.L >= 1) rec(d.L, 0);
+        bool hasL = false, Lallowed = false;
+        for (auto &dc : decomps) hasL |= dc.size() == 1 && dc[0] == d.L;
+        for (int s2 : sizes) Lallowed |= s2 == d.L;
+        if (!hasL && Lallowed) decomps.push_back({d.L});
+        // device support of a size, by sorted device index
+        auto supports = [&](int k, int size) {
+            const int dv = p.dev_order[k];
+            for (int c = d.batch_off[dv]; c < d.batch_off[dv + 1]; ++c)
+                if (d.batch_sizes[c] == size) return true;
+            return false;
+        };
+        std::vector<std::vector<int>> opt_sizes, opt_devs;
+        for (auto &dc : decomps) {
+            const int r = (int)dc.size();
+            std::vector<int> perm;
+            std::vector<char> used(K, 0);
+            std::function<void()> gen = [&]() {  // itertools.permutations order
+                if ((int)perm.size() == r) {
+                    for (int k = 0; k < r; ++k)
+                        if (!supports(perm[k], dc[k])) return;
+                    opt_sizes.push_back(dc);
+                    opt_devs.push_back(perm);
+                    return;
+                }
+                for (int k = 0; k < K; ++k) {
+                    if (used[k]) continue;
+                    used[k] = 1;
+                    perm.push_back(k);
+                    gen();
+                    perm.pop_back();
+                    used[k] = 0;
+                    if (opt_sizes.size() > 255) return;
+                }
+            };
+            gen();
+            if (opt_sizes.size() > 255)
+                return fail(err, HS_EINVAL, "more than 255 batched options "
+                                            "(uint8 extended genes)");
+        }
+        p.n_opt = (int)opt_sizes.size();
+        p.P = 1;
+        for (auto &o : opt_sizes) p.P = std::max(p.P, (int)o.size());
+        if (p.P > 8) return fail(err, HS_EINVAL, "more than 8 sub-batches per task");
+        const int P = p.P, NO = p.n_opt;
+        p.opt_np.assign(NO, 0);
+        p.opt_tab.assign(size_t(NO) * P * 4, -1);
+        for (int o = 0; o < NO; ++o) {
+            p.opt_np[o] = (int)opt_sizes[o].size();
+            int lo = 1;
+            for (int k = 0; k < p.opt_np[o]; ++k) {
+                int32_t *q = &p.opt_tab[(size_t(o) * P + k) * 4];
+                q[0] = opt_devs[o][k];
+                q[1] = lo;
+                q[2] = lo + opt_sizes[o][k] - 1;
+                q[3] = opt_sizes[o][k];
+                lo += opt_sizes[o][k];
+            }
+        }
+        p.bdur.assign(size_t(V) * NO * P, 0.0);
+        p.bdur_ok.assign(size_t(V) * NO * P, 0);
+        for (int i = 0; i < V; ++i) {
+            const int t = p.order[i];
+            for (int o = 0; o < NO; ++o)
+                for (int k = 0; k < p.opt_np[o]; ++k) {
+                    const int32_t *q = &p.opt_tab[(size_t(o) * P + k) * 4];
+                    const int dv = p.dev_order[q[0]];
+                    for (int c = d.batch_off[dv]; c < d.batch_off[dv + 1]; ++c)
+                        if (d.batch_sizes[c] == q[3] && lat_ok(t, c)) {
+                            const size_t at = (size_t(i) * NO + o) * P + k;
+                            p.bdur[at] = lat(t, c);
+                            p.bdur_ok[at] = 1;
+                            if (std::isnan(p.bdur[at])) p.nan_possible = true;
+                        }
+                }
+        }
+        // class tables are needed even for one bandwidth
+        if (p.ctab.empty()) {
+            p.ctab.assign(size_t(V) * p.n_cls, 0.0);
+            for (int i = 0; i < V; ++i)
+                for (int c = 1; c < p.n_cls; ++c)
+                    p.ctab[size_t(i) * p.n_cls + c] = d.om[p.order[i]] / beta_val[c - 1];
+        }
+        for (double x : p.ctab)
+            if (std::isnan(x)) p.nan_possible = true;
+    }
+
     // ---- blob layout (host image; slots are re-scaled per device config)
     DevLayout &L = p.lay;
     int64_t off = 0;
@@ -343,6 +460,10 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err) {
     L.bclass = put(int64_t(p.bclass.size()));
     L.cap = put(int64_t(K) * 8);
     L.okL = put(int64_t(K));
+    L.bopt = put(int64_t(p.opt_tab.size()) * 4);
+    L.bnp = put(int64_t(p.opt_np.size()) * 4);
+    L.bdur = put(int64_t(p.bdur.size()) * 8);
+    L.bdur_ok = put(int64_t(p.bdur_ok.size()));
     L.eval_bytes = off;
     L.cp_fast = put(int64_t(V) * 8);
     L.cp_fast_ok = put(int64_t(V));
@@ -368,6 +489,10 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err) {
     cpy(L.bclass, p.bclass.data(), p.bclass.size());
     cpy(L.cap, p.cap.data(), p.cap.size() * 8);
     cpy(L.okL, p.okL.data(), p.okL.size());
+    cpy(L.bopt, p.opt_tab.data(), p.opt_tab.size() * 4);
+    cpy(L.bnp, p.opt_np.data(), p.opt_np.size() * 4);
+    cpy(L.bdur, p.bdur.data(), p.bdur.size() * 8);
+    cpy(L.bdur_ok, p.bdur_ok.data(), p.bdur_ok.size());
     cpy(L.cp_fast, p.cp_fast.data(), p.cp_fast.size() * 8);
     cpy(L.cp_fast_ok, p.cp_fast_ok.data(), p.cp_fast_ok.size());
     cpy(L.cp_task, p.bfs.data(), p.bfs.size() * 4);

@@ -60,6 +60,15 @@ struct Plan {
     // ---- reachability (task insertion index)
     std::vector<int32_t> rc_succ_off, rc_succ, rc_pred_off, rc_pred;
 
+    // ---- batched variants (heuristics.py:337-433): extended genomes, one
+    // option (decomposition of L x distinct devices) per genome position
+    bool batched = false;
+    int n_opt = 0, P = 1;
+    std::vector<int32_t> opt_np;    // [n_opt]
+    std::vector<int32_t> opt_tab;   // [n_opt][P][4] = dev, lo, hi, size
+    std::vector<double> bdur;       // [V][n_opt][P]
+    std::vector<uint8_t> bdur_ok;   // [V][n_opt][P]
+
     DevLayout lay{};
     std::vector<uint8_t> blob;        // host image of the device blob
 
@@ -92,8 +101,16 @@ struct DevState {
     int kt = 0;               // K template (2,3,4) or 0 = generic K
 };
 
+// Batched-variant options: allowed sub-batch sizes (null = L/4, L/2, 3L/4,
+// L where integral, heuristics.py:337-342).
+struct BatchedSpec {
+    const int32_t *splits = nullptr;
+    int n_splits = 0;
+};
+
 // Builds the plan; on failure returns an HS_E* code and sets *err.
-int build_plan(const hs_instance_desc &d, Plan &p, std::string *err);
+int build_plan(const hs_instance_desc &d, Plan &p, std::string *err,
+               const BatchedSpec *batched = nullptr);
 
 // Device state for the current device (configures + uploads on first use).
 int get_dev_state(const Plan &p, const DevState **out, std::string *err);

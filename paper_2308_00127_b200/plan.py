@@ -47,7 +47,11 @@ class Plan:
     """Native evaluation plan of one instance at load L."""
 
     def __init__(self, g, hw, table, L: int,
-                 order: Optional[Sequence[str]] = None):
+                 order: Optional[Sequence[str]] = None,
+                 batched: Optional[tuple] = None):
+        """`batched` (a tuple of allowed sub-batch sizes, () = the
+        reference's default L/4, L/2, 3L/4, L) makes a batched-variant plan
+        whose genes are option indices (heuristics.py:337-433)."""
         lib = N.load()
         task_ids = list(g.tasks)
         tix = {t: k for k, t in enumerate(task_ids)}
@@ -103,7 +107,13 @@ class Plan:
         if K == 0:
             raise GraphError("gene value out of device range")
         h = C.c_void_p()
-        N.check(lib.hs_plan_create(C.byref(d), C.byref(h)), "plan")
+        if batched is None:
+            N.check(lib.hs_plan_create(C.byref(d), C.byref(h)), "plan")
+        else:
+            sp = np.array(list(batched) or [0], np.int32)
+            N.check(lib.hs_plan_create_batched(
+                C.byref(d), sp.ctypes.data if batched else None, len(batched),
+                C.byref(h)), "plan")
         self._keep = None
         self.handle = h
         self._lib = lib
@@ -119,6 +129,18 @@ class Plan:
         self.devices = tuple(dev_ids[k] for k in dv)  # gene k -> device id
         self.pref_ld = info.pref_ld
         self.words = info.words
+        self.batched = batched is not None
+        self.options = None
+        if self.batched:
+            n_opt, P = info.batched_options, info.max_parts
+            tab = np.zeros(max(n_opt * P * 4, 1), np.int32)
+            N.check(lib.hs_plan_batched_options(h, None, None, tab.ctypes.data))
+            tab = tab[:n_opt * P * 4].reshape(n_opt, P, 4)
+            self.options = [
+                (tuple(int(x[3]) for x in tab[o] if x[0] >= 0),
+                 tuple(self.devices[int(x[0])] for x in tab[o] if x[0] >= 0))
+                for o in range(n_opt)]
+            self.max_parts = P
         self._reach = None
         self._lock = threading.Lock()
         self.specialized_ms = None
@@ -270,15 +292,17 @@ def _ref(o):
         return lambda o=o: o  # not weak-referenceable: hold it
 
 
-def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None
-             ) -> Plan:
-    """Cached plan for (g, hw, table, L, order); `order` None or equal to
-    the graph's BFS order selects the default plan."""
+def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None,
+             batched: Optional[tuple] = None) -> Plan:
+    """Cached plan for (g, hw, table, L, order[, batched splits]); `order`
+    None or equal to the graph's BFS order selects the default plan."""
     if order is not None:
         order = tuple(order)
         if order == tuple(g._topo):
             order = None
-    key = (id(g), id(hw), id(table), int(L), order)
+    if batched is not None:
+        batched = tuple(sorted(set(int(x) for x in batched)))
+    key = (id(g), id(hw), id(table), int(L), order, batched)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None:
@@ -287,7 +311,7 @@ def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None
                 _CACHE.move_to_end(key)
                 return plan
             del _CACHE[key]
-    plan = Plan(g, hw, table, L, order)
+    plan = Plan(g, hw, table, L, order, batched)
     with _CACHE_LOCK:
         _CACHE[key] = ((_ref(g), _ref(hw), _ref(table)), plan)
         while len(_CACHE) > _CACHE_MAX:

@@ -409,6 +409,40 @@ def heur_doc():
     return out
 
 
+# ----------------------------------------------------------- batched variants
+def batched_doc():
+    """bMET / bGreedy schedules (heuristics.py:363-433, non-insertion) whose
+    per-task (decomposition, devices) choices form extended genomes."""
+    from conftest import random_instance
+    from hetsched.heuristics import batched_variant
+    out = []
+    cases = []
+    for s in range(60):
+        cases.append((f"ri_{s}_L2", random_instance(
+            4000 + s, max_tasks=6, max_devices=3, L=2), 2))
+    for s in range(30):
+        cases.append((f"ri_{s}_L4", random_instance(
+            5000 + s, max_tasks=6, max_devices=3, L=4), 4))
+    g = benchgen.gen_module("ws", 30, seed=0, k=4, p=0.75)
+    t, hw = benchgen.synth_profile(g, benchgen.DEFAULT3, seed=0)
+    cases += [("ws30_L4", (g, hw, t), 4), ("ws30_L8", (g, hw, t), 8),
+              ("ws30_L2", (g, hw, t), 2)]
+    for name, (g, hw, t), L in cases:
+        e = {"name": name, "L": L, **{k: v for k, v in inst_doc(
+            name, "", g, hw, t).items() if k not in ("name", "source")}}
+        for algo in ("met", "greedy"):
+            try:
+                s = batched_variant(algo, g, hw, t, L)
+                e[algo] = {"objective": fhex(s.objective),
+                           "batches": [[b.task, b.device, b.size,
+                                        list(b.inputs), fhex(b.start)]
+                                       for b in s.batches]}
+            except (ScheduleError, GraphError) as exc:
+                e[algo] = {"error": type(exc).__name__}
+        out.append(e)
+    return out
+
+
 def dump(path, obj):
     with open(path, "w") as f:
         json.dump(obj, f, separators=(",", ":"))
@@ -433,6 +467,7 @@ def main():
         dump(os.path.join(HERE, "random_instances.json"), mini_entries(pool))
     dump(os.path.join(HERE, "bounds.json"), bounds_doc(insts))
     dump(os.path.join(HERE, "heuristics.json"), heur_doc())
+    dump(os.path.join(HERE, "batched.json"), batched_doc())
 
 
 if __name__ == "__main__":

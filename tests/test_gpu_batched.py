@@ -1,0 +1,93 @@
+"""Extended-genome (batched-variant) evaluator against the reference's own
+bMET / bGreedy schedules and the pinned oracle restatement."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import fhex, golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2308_00127_b200 as hs  # noqa: E402
+from paper_2308_00127_b200 import _native as N  # noqa: E402
+from paper_2308_00127_b200.core import Schedule, ScheduledBatch  # noqa: E402
+from paper_2308_00127_b200.plan import get_plan  # noqa: E402
+from oracle import hs_batched as B  # noqa: E402
+from oracle import hs_oracle as O  # noqa: E402
+
+
+def test_reference_batched_schedules():
+    checked = 0
+    for e in golden("batched"):
+        g, hw, t = hs.load_instance(e)
+        L = e["L"]
+        for algo in ("met", "greedy"):
+            res = e[algo]
+            if "error" in res:
+                continue
+            ref = Schedule(batches=tuple(
+                ScheduledBatch(task=b[0], device=b[1], size=b[2],
+                               inputs=tuple(b[3]), start=float.fromhex(b[4]))
+                for b in res["batches"]), objective=0.0, input_count=L)
+            genes = hs.batched_genes_from_schedule(ref, g, hw, t, L)
+            s = hs.decode_batched(genes, g, hw, t, L)
+            assert fhex(s.objective) == res["objective"]
+            got = [[b.task, b.device, b.size, list(b.inputs), fhex(b.start)]
+                   for b in s.batches]
+            assert got == res["batches"]
+            ms = hs.fitness_batched(np.array([genes], np.uint8), g, hw, t, L)
+            assert fhex(ms[0]) == res["objective"]
+            checked += 1
+    assert checked > 150
+
+
+def test_random_extended_genomes_vs_oracle():
+    served = 0
+    for e in golden("batched"):
+        g, hw, t = hs.load_instance(e)
+        L = e["L"]
+        inst = O.Instance.from_doc(e)
+        opts = B.options(inst, L)
+        if not opts:
+            continue
+        rng = np.random.default_rng(served)
+        genes = rng.integers(len(opts), size=(200, len(g.tasks)),
+                             dtype=np.uint8)
+        genes[0, 0] = len(opts)  # out of range -> GraphError status
+        want = [B.eval_one(inst, L, opts, row) for row in genes]
+        ms, st = hs.fitness_batched(torch.from_numpy(genes).cuda(), g, hw, t,
+                                    L, return_status=True)
+        ms, st = ms.cpu().numpy(), st.cpu().numpy()
+        for r, (wm, ws) in enumerate(want):
+            assert st[r] == ws, (e["name"], r)
+            if ws == 0:
+                assert ms[r] == wm, (e["name"], r)
+        hm, hst = hs.fitness_batched(genes, g, hw, t, L, return_status=True)
+        assert np.array_equal(hst, st)
+        ok = st == 0
+        assert np.array_equal(hm[ok], ms[ok])
+        served += 1
+    assert served > 60
+
+
+def test_generated_extended_genomes():
+    e = [x for x in golden("batched") if x["name"] == "ws30_L4"][0]
+    g, hw, t = hs.load_instance(e)
+    inst = O.Instance.from_doc(e)
+    opts = B.options(inst, 4)
+    plan = get_plan(g, hw, t, 4, None, ())
+    n = 3000
+    out = torch.empty((n, plan.V), dtype=torch.uint8, device="cuda")
+    ms = torch.empty(n, dtype=torch.float64, device="cuda")
+    plan.eval_gen(N.GEN_RANDOM, 3, 10, n, makespan=ms, genes_out=out)
+    genes = O.gen_genes(3, 10, n, plan.V, len(opts))
+    assert np.array_equal(out.cpu().numpy(), genes)
+    want = np.array([B.eval_one(inst, 4, opts, r)[0] for r in genes])
+    assert np.array_equal(ms.cpu().numpy(), want)
+    cost, idx, best = hs.random_search_batched(g, hw, t, 4, n + 10, seed=3)
+    allg = O.gen_genes(3, 0, n + 10, plan.V, len(opts))
+    allw = np.array([B.eval_one(inst, 4, opts, r)[0] for r in allg])
+    assert (cost, idx) == O.argmin_first(allw)
+    assert best == [int(x) for x in allg[idx]]

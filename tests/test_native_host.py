@@ -87,3 +87,15 @@ def test_live_slots_are_small_for_stacks():
     assert p.info.live_slots == 2 and p.info.n_classes == 2
     p = Plan(*hs.load_instance(instance_doc("ws200")), 1)
     assert p.info.live_slots == 101 and p.info.uniform_comm == 1
+
+
+def test_batched_options_match_reference_enumeration():
+    from conftest import golden
+    from oracle import hs_batched as B
+    from oracle import hs_oracle as O
+    for e in golden("batched"):
+        g, hw, t = hs.load_instance(e)
+        inst = O.Instance.from_doc(e)
+        want = [(s, tuple(sorted(inst.dev_ids)[k] for k in dv))
+                for s, dv in B.options(inst, e["L"])]
+        assert hs.batched_options(g, hw, t, e["L"]) == want

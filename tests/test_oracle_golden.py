@@ -112,3 +112,24 @@ def test_search_oracle_golden():
                 run["mapping"]
             checked += 1
     assert checked > 50
+
+
+def test_batched_oracle_golden():
+    """The extended-genome restatement reproduces the reference's bMET and
+    bGreedy schedules (objective and every sub-batch start)."""
+    from oracle import hs_batched as B
+    checked = 0
+    for e in golden("batched"):
+        inst = O.Instance.from_doc(e)
+        opts = B.options(inst, e["L"])
+        for algo in ("met", "greedy"):
+            res = e[algo]
+            if "error" in res:
+                continue
+            genes = B.genes_from_schedule(inst, e["L"], opts, res["batches"])
+            ms, st, starts = B.eval_one(inst, e["L"], opts, genes, trace=True)
+            assert st == 0 and fhex(ms) == res["objective"]
+            got = [fhex(x) for row in starts for x in row]
+            assert got == [b[4] for b in res["batches"]]
+            checked += 1
+    assert checked > 150
