@@ -250,8 +250,11 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err,
             if (last_use[i] >= 0) dies[last_use[i]].push_back(i);
         for (int i = 0; i < V; ++i) {
             // predecessors whose last reader is i are read before i's end
-            // is written, so their slots can be recycled for i
-            for (int q : dies[i]) freel.push(slot[q]);
+            // is written, so their slots can be recycled for i -- except
+            // in batched plans, where part k's end is written before part
+            // k+1 reads the predecessors
+            if (!bspec)
+                for (int q : dies[i]) freel.push(slot[q]);
             if (last_use[i] >= 0) {
                 if (!freel.empty()) {
                     slot[i] = freel.top();
@@ -260,6 +263,8 @@ int build_plan(const hs_instance_desc &d, Plan &p, std::string *err,
                     slot[i] = next++;
                 }
             }
+            if (bspec)
+                for (int q : dies[i]) freel.push(slot[q]);
         }
         p.live_slots = next;
     }
