@@ -104,6 +104,12 @@ __device__ __forceinline__ double pymax(double a, double b) {
     return b > a ? b : a;  // Python max(a, b): a unless b > a
 }
 
+// Python max(a, b) for a, b >= +0.0 and not NaN: the binary64 bit patterns
+// of non-negative doubles order like the values (ALU compare, not FP64)
+__device__ __forceinline__ double pymax_nn(double a, double b) {
+    return __double_as_longlong(b) > __double_as_longlong(a) ? b : a;
+}
+
 // branch-free select (kept as FSEL pairs: the specialised code relies on it
 // to stay divergence free when lanes map tasks to different devices)
 __device__ __forceinline__ double dsel(bool p, double a, double b) {

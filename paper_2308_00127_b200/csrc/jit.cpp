@@ -112,6 +112,7 @@ JitOpts JitOpts::from_env() {
             if (k == "win") o.reg_window = std::atoi(v.c_str());
             if (k == "avail") o.avail_smem = v == "smem";
             if (k == "dur") o.dur_smem = v == "smem";
+            if (k == "max") o.int_max = v == "int";
         }
         at = end + 1;
     }
@@ -174,8 +175,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         std::string &s = *src;
         s.clear();
         s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
-        s += "struct JitBody {\n  double *ends; double *avail; const double *dur; "
-             "double *starts;\n";
+        s += "template <bool TRACE>\nstruct JitBody {\n  double *ends; double *avail; "
+             "const double *dur; double *starts;\n";
         s += "  __device__ __forceinline__ void run(const hs_u8 *g, int li, "
              "hs_i64 cand, bool valid, double &ms_out, int &st_out) {\n";
         s += "    double *E = ends + li;\n";
@@ -188,6 +189,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 s += "    double a" + std::to_string(k) + " = 0.0;\n";
         }
         s += "    int gmax = 0;\n";
+        // no NaN and no negative times inside the specialised scope: max on
+        // the binary64 bit patterns equals Python's max (ALU, not FP64)
+        const std::string mx = o.int_max ? "pymax_nn" : "pymax";
         char buf[1024];
         for (int i = 0; i < V; ++i) {
             const std::string di = "d" + std::to_string(i);
@@ -231,7 +235,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                     for (size_t k = 0; k + 1 < xs.size(); k += 2) {
                         const std::string m = "m" + std::to_string(i) + "_" +
                                               std::to_string(lvl) + "_" + std::to_string(k);
-                        s += "    const double " + m + " = pymax(" + xs[k] + ", " +
+                        s += "    const double " + m + " = " + mx + "(" + xs[k] + ", " +
                              xs[k + 1] + ");\n";
                         nx.push_back(m);
                     }
@@ -251,9 +255,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             const std::string Ai = "A" + std::to_string(i);
             if (o.avail_smem) {
                 s += "    double *" + Ai + " = A + " + di + " * " + std::to_string(T) + ";\n";
-                s += "    const double " + si + " = pymax(" + r + ", *" + Ai + ");\n";
+                s += "    const double " + si + " = " + mx + "(" + r + ", *" + Ai + ");\n";
             } else {
-                s += "    const double " + si + " = pymax(" + r + ", " + sel(di, av) + ");\n";
+                s += "    const double " + si + " = " + mx + "(" + r + ", " + sel(di, av) + ");\n";
             }
             std::string dsrc = sel(di, du);
             if (o.dur_smem && dsrc != du[0])
@@ -261,7 +265,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             const std::string ei = "e" + std::to_string(i);
             s += "    const double " + ei + " = " + si + " + " + dsrc + ";\n";
             std::snprintf(buf, sizeof buf,
-                          "    if (starts && valid) starts[cand * %d + %d] = %s;\n", V, i,
+                          "    if (TRACE && valid) starts[cand * %d + %d] = %s;\n", V, i,
                           si.c_str());
             s += buf;
             if (where[i] >= 0)
@@ -284,16 +288,13 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                       "    const int st = gmax >= %d ? ST_GENE : ST_OK;\n"
                       "    ms_out = st ? knan() : ms;\n    st_out = st;\n  }\n};\n", K);
         s += buf;
-        std::snprintf(buf, sizeof buf,
-                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
-                      "hs_jit_eval(const EvalParams a) {\n"
-                      "  extern __shared__ __align__(16) hs_u8 smem[];\n"
-                      "  JitBody body;\n"
-                      "  body.ends = reinterpret_cast<double *>(smem + a.smem_ends);\n"
-                      "  body.avail = reinterpret_cast<double *>(smem + a.smem_kstate);\n"
-                      "  body.dur = reinterpret_cast<const double *>(smem + 16);\n"
-                      "  body.starts = a.starts;\n", T);
-        s += buf;
+        s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
+             "  extern __shared__ __align__(16) hs_u8 smem[];\n"
+             "  JitBody<TRACE> body;\n"
+             "  body.ends = reinterpret_cast<double *>(smem + a.smem_ends);\n"
+             "  body.avail = reinterpret_cast<double *>(smem + a.smem_kstate);\n"
+             "  body.dur = reinterpret_cast<const double *>(smem + 16);\n"
+             "  body.starts = a.starts;\n";
         if (o.dur_smem) {
             std::snprintf(buf, sizeof buf,
                           "  { const uint4 *src = reinterpret_cast<const uint4 *>(a.blob + "
@@ -303,6 +304,12 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             s += buf;
         }
         s += "  eval_tiles(a, smem, body);\n}\n";
+        std::snprintf(buf, sizeof buf,
+                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                      "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
+                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                      "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n", T, T);
+        s += buf;
         return next;
     }
 }
@@ -372,6 +379,10 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0,
                                         nullptr, nullptr, 0);
     if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern, m->lib, "hs_jit_eval");
+    if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern_trace, m->lib, "hs_jit_trace");
+    if (e == cudaSuccess)
+        e = cudaKernelSetAttributeForDevice(
+            m->kern_trace, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
     if (e == cudaSuccess)
         e = cudaKernelSetAttributeForDevice(
             m->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
@@ -402,7 +413,8 @@ void jit_free(JitModule *m) {
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid, cudaStream_t stream,
                std::string *err) {
     void *args[] = {(void *)&a};
-    cudaError_t e = cudaLaunchKernel((const void *)m.kern, dim3(grid), dim3(m.T), args,
+    const cudaKernel_t k = a.starts ? m.kern_trace : m.kern;
+    cudaError_t e = cudaLaunchKernel((const void *)k, dim3(grid), dim3(m.T), args,
                                      m.smem, stream);
     if (e != cudaSuccess) {
         if (err) *err = std::string("specialised eval launch: ") + cudaGetErrorString(e);

@@ -17,13 +17,14 @@ struct JitOpts {
     int reg_window = 400;  // ... when consumed within this many positions
     bool avail_smem = true;   // per-device available times in shared memory
     bool dur_smem = true;     // latency table in shared memory (else selects)
+    bool int_max = false;     // max via int64 compare of bit patterns
     static JitOpts from_env();
 };
 
 struct JitModule {
     int device = -1;
     cudaLibrary_t lib = nullptr;
-    cudaKernel_t kern = nullptr;
+    cudaKernel_t kern = nullptr, kern_trace = nullptr;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;
     int64_t smem_tile = 0, smem_ends = 0, smem_kstate = 0;
