@@ -154,6 +154,17 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
                  int64_t ld, double *h_makespan, uint8_t *h_status,
                  hs_best *h_best, int64_t index_base, void *stream);
 
+/* 2-bit packed genomes (K <= 4, or <= 4 batched options): gene i of a row
+ * is bits 2*(i%4)..2*(i%4)+1 of byte i/4; rows of `ld` bytes with ld % 4
+ * == 0 and ceil(V/4) <= ld <= pref_ld. A quarter of the bytes of hs_eval's
+ * input (the host path is PCIe-bound); expanded in shared memory. */
+int hs_eval_packed(const hs_plan *plan, const uint8_t *d_packed, int64_t n,
+                   int64_t ld, double *d_makespan, uint8_t *d_status,
+                   hs_best *d_best, int64_t index_base, void *stream);
+int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
+                        int64_t ld, double *h_makespan, uint8_t *h_status,
+                        hs_best *h_best, int64_t index_base, void *stream);
+
 /* On-device candidates: candidate c in [first, first+n) has genes
  * oracle/hs_oracle.py::gen_genes(seed, c). Optional d_genes_out [n x V]. */
 int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,

@@ -15,7 +15,8 @@ from .core import (Device, DnnGraph, GraphError, HardwareSystem,
                    save_hardware, save_latency, save_schedule,
                    transitive_closure)
 from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
-                         fitness, fitness_batch, genome_from_map, greedy, met,
+                         fitness, fitness_batch, fitness_batch_packed,
+                         genome_from_map, greedy, met, pack_genes,
                          one_plus_one_ea, random_search, simulated_annealing,
                          specialize, throughput)
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,

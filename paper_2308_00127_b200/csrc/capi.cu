@@ -178,12 +178,22 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
              int gen, uint64_t seed, int64_t first, const uint8_t *tmpl,
              const int16_t *group, int n_groups, double *makespan,
              uint8_t *status, double *starts, uint8_t *genes_out, hs_best *best,
-             int64_t index_base, cudaStream_t stream) {
+             int64_t index_base, cudaStream_t stream, int packed = 0) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
     const hs::Plan &p = plan->p;
     if (n < 0) return set_err(HS_EINVAL, "n < 0");
-    if (!gen && n > 0 && p.V > 0 && (!genes || ld < p.V))
+    if (packed) {
+        // 2-bit genes: rows of ld bytes, ld a multiple of 4, >= ceil(V/4),
+        // at most the staged tile row (expanded in place)
+        if (p.batched ? p.n_opt > 4 : p.K > 4)
+            return set_err(HS_EINVAL, "2-bit packed genomes need at most 4 gene values");
+        if (n > 0 && p.V > 0 &&
+            (!genes || ld % 4 || ld * 4 < p.V || ld > p.pref_ld() || ld > 256))
+            return set_err(HS_EINVAL, "packed genes must be [n x ld], ld % 4 == 0, "
+                                      "4*ld >= V, ld <= preferred stride");
+    } else if (!gen && n > 0 && p.V > 0 && (!genes || ld < p.V)) {
         return set_err(HS_EINVAL, "genes must be [n x ld] with ld >= V");
+    }
     const hs::DevState *ds = nullptr;
     std::string err;
     int rc = hs::get_dev_state(p, &ds, &err);
@@ -195,7 +205,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
 
     Scratch repack;
     repack.s = stream;
-    if (!gen && n > 0 && ld > ds->ld_cap) {
+    if (!gen && !packed && n > 0 && ld > ds->ld_cap) {
         // exotic row stride: compact to the preferred stride first
         const int64_t pl = p.pref_ld();
         CK(cudaMallocAsync(&repack.ptr, size_t(n * pl), stream));
@@ -234,7 +244,8 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.flags = flags_of(p);
     a.plan_smem = ds->plan_smem ? 1 : 0;
     a.lanes = lanes;
-    a.ld_s = gen ? p.pref_ld() : int(ld);
+    a.ld_s = (gen || packed) ? p.pref_ld() : int(ld);
+    a.packed = packed;
     a.slots = p.live_slots;
     a.bulk = (!gen && (reinterpret_cast<uintptr_t>(genes) & 15) == 0) ? 1 : 0;
     a.genes = genes;
@@ -407,6 +418,14 @@ int hs_eval(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
                     static_cast<cudaStream_t>(stream));
 }
 
+int hs_eval_packed(const hs_plan *plan, const uint8_t *d_packed, int64_t n,
+                   int64_t ld, double *d_makespan, uint8_t *d_status,
+                   hs_best *d_best, int64_t index_base, void *stream) {
+    return run_eval(plan, d_packed, n, ld, 0, 0, 0, nullptr, nullptr, 0, d_makespan,
+                    d_status, nullptr, nullptr, d_best, index_base,
+                    static_cast<cudaStream_t>(stream), 1);
+}
+
 int hs_eval_gen_ex(const hs_plan *plan, int mode, uint64_t seed, int64_t first,
                    int64_t n, const uint8_t *d_template, const int16_t *d_group,
                    int32_t n_groups, double *d_makespan, uint8_t *d_status,
@@ -465,9 +484,10 @@ constexpr int64_t kSmallN = 1 << 16;
 
 int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
                     int64_t ld, double *h_makespan, uint8_t *h_status,
-                    hs_best *h_best, int64_t index_base, cudaStream_t s) {
-    const int64_t V = plan->p.V;
-    const int64_t lds = plan->p.pref_ld();  // compact, TMA-friendly stride
+                    hs_best *h_best, int64_t index_base, cudaStream_t s,
+                    int packed) {
+    const int64_t V = packed ? ld : plan->p.V;  // bytes of a row
+    const int64_t lds = packed ? ld : plan->p.pref_ld();  // TMA-friendly stride
     const size_t gb = (size_t(n * lds) + 255) & ~size_t(255);
     const size_t need = gb + size_t(n) * 9 + 64;
     int dev = 0;
@@ -490,7 +510,7 @@ int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     hs_best *db = reinterpret_cast<hs_best *>(w.d + ((gb + size_t(n) * 9 + 15) & ~size_t(15)));
     CK(cudaMemcpyAsync(w.d, w.h, size_t(n * lds), cudaMemcpyHostToDevice, s));
     int rc = run_eval(plan, w.d, n, lds, 0, 0, 0, nullptr, nullptr, 0, dm, dst,
-                      nullptr, nullptr, h_best ? db : nullptr, index_base, s);
+                      nullptr, nullptr, h_best ? db : nullptr, index_base, s, packed);
     if (rc) return rc;
     // results come back contiguously: makespans, statuses, best
     const size_t back = (reinterpret_cast<uint8_t *>(db) - reinterpret_cast<uint8_t *>(dm)) +
@@ -508,16 +528,17 @@ int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
 
 }  // namespace
 
-int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
-                 int64_t ld, double *h_makespan, uint8_t *h_status,
-                 hs_best *h_best, int64_t index_base, void *stream) {
+static int eval_host_impl(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
+                          int64_t ld, double *h_makespan, uint8_t *h_status,
+                          hs_best *h_best, int64_t index_base, void *stream,
+                          int packed) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
-    if (n < 0 || (n > 0 && (!h_genes || ld < plan->p.V)))
+    if (n < 0 || (n > 0 && (!h_genes || (!packed && ld < plan->p.V))))
         return set_err(HS_EINVAL, "genes must be [n x ld] with ld >= V");
     cudaStream_t s0 = static_cast<cudaStream_t>(stream);
     if (n > 0 && n <= kSmallN && plan->p.V > 0)
         return eval_host_small(plan, h_genes, n, ld, h_makespan, h_status, h_best,
-                               index_base, s0);
+                               index_base, s0, packed);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 1 << 19));
     const int64_t nchunks = n > 0 ? (n + chunk - 1) / chunk : 1;
     const size_t gbytes = size_t(chunk * ld);
@@ -561,7 +582,7 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
             rc = run_eval(plan, dg, std::max<int64_t>(rows, 0), ld, 0, 0, 0,
                           nullptr, nullptr, 0, h_makespan ? dm : nullptr, h_status ? dsx : nullptr,
                           nullptr, nullptr, h_best ? bests + c : nullptr,
-                          index_base + lo, s);
+                          index_base + lo, s, packed);
             if (rc) break;
             if (h_makespan && rows > 0)
                 e = cudaMemcpyAsync(h_makespan + lo, dm, size_t(rows) * 8,
@@ -592,6 +613,20 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     return rc;
+}
+
+int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
+                 int64_t ld, double *h_makespan, uint8_t *h_status,
+                 hs_best *h_best, int64_t index_base, void *stream) {
+    return eval_host_impl(plan, h_genes, n, ld, h_makespan, h_status, h_best,
+                          index_base, stream, 0);
+}
+
+int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
+                        int64_t ld, double *h_makespan, uint8_t *h_status,
+                        hs_best *h_best, int64_t index_base, void *stream) {
+    return eval_host_impl(plan, h_packed, n, ld, h_makespan, h_status, h_best,
+                          index_base, stream, 1);
 }
 
 int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,

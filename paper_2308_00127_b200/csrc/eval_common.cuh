@@ -74,6 +74,7 @@ struct EvalParams {
     int plan_smem;
     int lanes, ld_s, slots;
     int bulk;           // genome tiles may use cp.async.bulk
+    int packed;         // genes arrive 2 bits each (K <= 4), `ld` bytes/row
     const hs_u8 *genes;
     hs_i64 n, ld;
     int gen;            // 1 hash-random, 2 enumerate (K6); 0 staged genes
@@ -302,12 +303,41 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
         } else {
             const hs_i64 bytes = (hs_i64)rows * a.ld;
             const hs_u8 *src = a.genes + c0 * a.ld;
+            // packed rows land in the last bytes of the tile and are
+            // expanded in place (all rows read before any row is written)
+            hs_u8 *dst = a.packed ? gtile + (hs_i64)lanes * a.ld_s - (hs_i64)lanes * a.ld
+                                  : gtile;
             if (a.bulk && bytes > 0 && (bytes & 15) == 0) {
-                if (tid == 0) bulk_g2s(gtile, src, (hs_u32)bytes, bar);
+                if (tid == 0) bulk_g2s(dst, src, (hs_u32)bytes, bar);
                 mbar_wait(bar, phase);
                 phase ^= 1u;
             } else {
-                for (hs_i64 b = tid; b < bytes; b += T) gtile[b] = src[b];
+                for (hs_i64 b = tid; b < bytes; b += T) dst[b] = src[b];
+            }
+            if (a.packed) {
+                __syncthreads();
+                // 2-bit genes, 16 per word: word w -> four 4-gene words
+                hs_u32 pk[64];
+                const int nw = (int)(a.ld >> 2);
+                const hs_u32 *prow = reinterpret_cast<const hs_u32 *>(dst + (hs_i64)tid * a.ld);
+#pragma unroll 4
+                for (int w = 0; w < nw && w < 64; ++w) pk[w] = tid < rows ? prow[w] : 0u;
+                __syncthreads();
+                hs_u32 *orow = reinterpret_cast<hs_u32 *>(gtile + (hs_i64)tid * a.ld_s);
+                const int nout = a.ld_s >> 2;
+#pragma unroll 4
+                for (int w = 0; w < nw && w < 64; ++w) {
+                    const hs_u32 x = pk[w];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int o = 4 * w + j;
+                        if (o < nout) {
+                            const hs_u32 b = (x >> (8 * j)) & 0xFFu;
+                            orow[o] = (b & 3u) | ((b & 0xCu) << 6) | ((b & 0x30u) << 12) |
+                                      ((b & 0xC0u) << 18);
+                        }
+                    }
+                }
             }
         }
         __syncthreads();

@@ -219,6 +219,50 @@ def fitness_batch(genes, g, hw, table, L: int, *,
     return ms
 
 
+def pack_genes(genes: np.ndarray) -> np.ndarray:
+    """2-bit packing of uint8 genes < 4 [n, V] -> [n, ceil(ceil(V/4)/4)*4]:
+    gene i in bits 2*(i%4) of byte i//4 (hs_eval_packed's layout)."""
+    genes = np.asarray(genes, np.uint8)
+    n, V = genes.shape
+    if genes.size and genes.max() > 3:
+        raise GraphError("2-bit packing needs genes < 4")
+    pld = ((V + 3) // 4 + 3) // 4 * 4
+    g = np.zeros((n, pld * 4), np.uint8)
+    g[:, :V] = genes
+    g = g.reshape(n, pld, 4)
+    return (g[:, :, 0] | (g[:, :, 1] << 2) | (g[:, :, 2] << 4)
+            | (g[:, :, 3] << 6)).astype(np.uint8)
+
+
+def fitness_batch_packed(packed, g, hw, table, L: int, *,
+                         return_status: bool = False):
+    """fitness_batch for 2-bit packed genomes (pack_genes): numpy -> host
+    path (a quarter of the PCIe bytes), CUDA tensor -> device path."""
+    plan = get_plan(g, hw, table, L)
+    n = int(packed.shape[0])
+    plan.maybe_specialize(n)
+    if hasattr(packed, "data_ptr"):
+        import torch
+        ms = torch.empty(n, dtype=torch.float64, device=packed.device)
+        st = torch.empty(n, dtype=torch.uint8, device=packed.device)
+        plan.eval_packed(packed, ms, st)
+        if return_status:
+            return ms, st
+        if n and int(st.max().item()) >= N.ST_MISSING:
+            _raise_status(int(st.max().item()))
+        return ms
+    packed = np.ascontiguousarray(packed, np.uint8)
+    ms = np.empty(n, np.float64)
+    st = np.empty(n, np.uint8)
+    if n:
+        plan.eval_host_packed(packed, ms, st)
+    if return_status:
+        return ms, st
+    if n and st.max() >= N.ST_MISSING:
+        _raise_status(int(st.max()))
+    return ms
+
+
 def specialize(g, hw, table, L: int, order=None) -> float:
     """Compile the graph-specialised evaluator for this instance on the
     current device (csrc/jit.cpp); returns the compile time in ms."""

@@ -210,3 +210,29 @@ def test_enumeration_with_groups():
 def test_throughput_helper():
     assert list(hs.throughput(np.array([500.0, 0.0, np.inf]), 4)) == \
         [8.0, np.inf, 0.0]
+
+
+@pytest.mark.parametrize("name", ["ws200", "ws30", "rn50f"])
+def test_packed_genomes(name, oracle_lib):
+    doc = instance_doc(name)
+    g, hw, t = hs.load_instance(doc)
+    tb = O.build_tables(O.Instance.from_doc(doc), 1)
+    plan = get_plan(g, hw, t, 1)
+    for n in (1, 33, 5000, 200_000, -1):
+        if n < 0:  # once more through the graph-specialised kernel
+            plan.specialize()
+            n = 100_000
+        genes = np.random.default_rng(n).integers(plan.K, size=(n, plan.V),
+                                                  dtype=np.uint8)
+        genes[0, -1] = 3  # out of range for K = 3 -> GraphError status
+        want, wst = CTables(tb).fitness(oracle_lib, genes, threads=8)
+        packed = hs.pack_genes(genes)
+        for arg in (packed, torch.from_numpy(packed).cuda()):
+            ms, st = hs.fitness_batch_packed(arg, g, hw, t, 1,
+                                             return_status=True)
+            ms = ms.cpu().numpy() if hasattr(ms, "cpu") else ms
+            st = st.cpu().numpy() if hasattr(st, "cpu") else st
+            assert np.array_equal(st, wst)
+            ok = wst == 0
+            assert np.array_equal(ms[ok].view(np.uint64),
+                                  want[ok].view(np.uint64))
