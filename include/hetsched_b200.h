@@ -126,12 +126,12 @@ int hs_plan_batched_options(const hs_plan *plan, int32_t *n_opt,
                             int32_t *max_parts, int32_t *table);
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
 /* Specialise the evaluator to this plan on the current device: the plan is
- * emitted as straight-line CUDA and compiled by NVRTC for sm_100a (one-time
+ * emitted as straight-line CUDA (predecessor slots, communication and
+ * latency constants baked in) and compiled by NVRTC for sm_100a (one-time
  * cost, reported in *compile_ms); later hs_eval* calls on this device use
- * it. HS_EINVAL when the plan is outside the specialised scope (K <= 4,
- * one bandwidth over a full mesh, no capacity / batch-size / missing-entry
- * / NaN cases, V <= 512, E <= 2048); the ahead-of-time kernel then keeps
- * serving the plan. */
+ * it. HS_EINVAL when the plan is outside the specialised scope (batched
+ * plans, K > 64, V > 512, E > 2048, or a NaN in the cost model); the
+ * ahead-of-time kernel then keeps serving the plan. */
 int hs_plan_specialize(const hs_plan *plan, double *compile_ms);
 /* The CUDA source the specialiser would compile for `lanes` lanes. */
 int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,

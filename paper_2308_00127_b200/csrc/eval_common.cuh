@@ -120,6 +120,30 @@ __device__ __forceinline__ double dsel(bool p, double a, double b) {
     return r;
 }
 
+// Shared-memory accesses the optimiser cannot see through. The specialised
+// kernels keep per-device state at A + d * T (d = the lane's gene): if the
+// front end could relate those addresses it would rewrite the array into
+// K-way select chains per task -- super-linear compile time for K ~ 30.
+// No memory clobber: the regions accessed this way are accessed only this
+// way, so ordinary loads and stores may still be scheduled around them.
+__device__ __forceinline__ double ld_shared_f64(hs_u32 a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_shared_f64(hs_u32 a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+
+// branch-free status update: keep the first failing check's code (the
+// optimiser must not turn hundreds of these into nested branches)
+__device__ __forceinline__ int first_status(int st, bool fail, int code) {
+    int r;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n selp.b32 %0, %1, %3, q;\n}"
+        : "=r"(r) : "r"(code), "r"((int)(fail && st == 0)), "r"(st));
+    return r;
+}
+
 __device__ __forceinline__ bool best_less(double c1, hs_i64 i1, double c2, hs_i64 i2) {
     return c1 < c2 || (c1 == c2 && i1 < i2);
 }

@@ -119,25 +119,75 @@ JitOpts JitOpts::from_env() {
     return o;
 }
 
-static int64_t dur_bytes(const Plan &p) {
-    return (int64_t(p.V) * p.K * 8 + 15) & ~int64_t(15);
-}
+static int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 // Straight-line code grows with V + E and ptxas time super-linearly
 // (minutes at V ~ 1000), so very large graphs stay on the AOT kernel.
-constexpr int kJitMaxV = 512, kJitMaxE = 2048;
+constexpr int kJitMaxV = 512, kJitMaxE = 2048, kJitMaxK = 64;
 
 bool jit_eligible(const Plan &p) {
-    return !p.batched && p.K <= 4 && p.uniform_comm && !p.mem_check && p.all_batch_ok &&
-           p.latency_complete && !p.nan_possible && p.V > 0 &&
+    return !p.batched && p.K <= kJitMaxK && !p.nan_possible && p.V > 0 &&
            p.V <= kJitMaxV && p.E <= kJitMaxE;
 }
 
-// Emits the body for T lanes. Returns the number of shared-memory slots.
+namespace {
+
+// Shared-memory layout of the specialised kernel (byte offsets); every
+// table is staged from the plan blob once per CTA.
+struct JitLayout {
+    bool dur = false, cls = false, mem = false, avail = false;
+    int64_t dur_off = 0, ctab_off = 0, bcl_off = 0, cap_off = 0, head = 16;
+    int64_t tile = 0, ends = 0, avail_off = 0, mem_off = 0, total = 0;
+};
+
+JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap) {
+    JitLayout l;
+    l.dur = o.dur_smem || p.K > 4;
+    l.avail = o.avail_smem || p.K > 4;
+    l.cls = !p.uniform_comm;
+    l.mem = p.mem_check;
+    int64_t at = 16;
+    if (l.dur) { l.dur_off = at; at += a16(int64_t(p.V) * p.K * 8); }
+    if (l.cls) {
+        l.ctab_off = at; at += a16(int64_t(p.V) * p.n_cls * 8);
+        l.bcl_off = at; at += a16(int64_t(p.K) * p.K * 2);
+    }
+    if (l.mem) { l.cap_off = at; at += a16(int64_t(p.K) * 8); }
+    l.head = at;
+    l.tile = at;
+    l.ends = l.tile + a16(int64_t(T) * ld_cap);
+    at = l.ends + int64_t(slots) * T * 8;
+    if (l.avail) { l.avail_off = at; at += int64_t(p.K) * T * 8; }
+    if (l.mem) { l.mem_off = at; at += int64_t(p.K) * T * 8; }
+    l.total = at;
+    return l;
+}
+
+int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap) {
+    const bool avail = o.avail_smem || p.K > 4;
+    return ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
+}
+
+int64_t head_bytes(const Plan &p, const JitOpts &o) {
+    return jit_layout(p, o, 32, 0, 0).head;
+}
+
+std::string stage(int64_t dst, const char *section, int64_t bytes) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf,
+                  "  { const uint4 *src = reinterpret_cast<const uint4 *>(a.blob + a.lay.%s);\n"
+                  "    uint4 *dst = reinterpret_cast<uint4 *>(smem + %lld);\n"
+                  "    for (int q = threadIdx.x; q < %lld; q += blockDim.x) dst[q] = src[q]; }\n",
+                  section, (long long)dst, (long long)(a16(bytes) / 16));
+    return buf;
+}
+
+}  // namespace
+
+// Emits the kernel for T lanes; returns the number of shared-memory slots.
 int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     const int V = p.V, K = p.K;
     const int reg_budget = o.reg_budget, reg_window = o.reg_window;
-    // lifetimes in genome order
     std::vector<int> last(V, -1);
     std::vector<std::vector<int>> preds(V);  // positions
     for (int i = 0; i < V; ++i)
@@ -148,12 +198,13 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
     // register residency for short-lived end times, slots for the rest
     std::vector<int> where(V, -2);  // -2 none, -1 register, >=0 slot
+    int next = 0;
     {
         std::vector<std::vector<int>> dies(V);
         for (int i = 0; i < V; ++i)
             if (last[i] >= 0) dies[last[i]].push_back(i);
         std::priority_queue<int, std::vector<int>, std::greater<int>> freel;
-        int next = 0, live_regs = 0;
+        int live_regs = 0;
         for (int i = 0; i < V; ++i) {
             for (int q : dies[i]) {
                 if (where[q] >= 0) freel.push(where[q]);
@@ -170,148 +221,211 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 where[i] = next++;
             }
         }
-        if (src == nullptr) return next;
-        (void)0;
-        std::string &s = *src;
-        s.clear();
-        s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
-        s += "template <bool TRACE>\nstruct JitBody {\n  double *ends; double *avail; "
-             "const double *dur; double *starts;\n";
-        s += "  __device__ __forceinline__ void run(const hs_u8 *g, int li, "
-             "hs_i64 cand, bool valid, double &ms_out, int &st_out) {\n";
-        s += "    double *E = ends + li;\n";
-        if (o.avail_smem) {
-            s += "    double *A = avail + li;\n";
-            for (int k = 0; k < K; ++k)
-                s += "    A[" + std::to_string(k * T) + "] = 0.0;\n";
-        } else {
-            for (int k = 0; k < K; ++k)
-                s += "    double a" + std::to_string(k) + " = 0.0;\n";
-        }
-        s += "    int gmax = 0;\n";
-        // no NaN and no negative times inside the specialised scope: max on
-        // the binary64 bit patterns equals Python's max (ALU, not FP64)
-        const std::string mx = o.int_max ? "pymax_nn" : "pymax";
-        char buf[1024];
-        for (int i = 0; i < V; ++i) {
-            const std::string di = "d" + std::to_string(i);
-            s += "    // " + p.task_ids[p.order[i]] + "\n";
-            // raw gene for the range check; clamped for table / state
-            // indexing (lanes past the last row read stale tile bytes)
-            std::snprintf(buf, sizeof buf,
-                          "    const int g%d = g[%d]; gmax = max(gmax, g%d);\n"
-                          "    const int %s = min(g%d, %d);\n",
-                          i, i, i, di.c_str(), i, K - 1);
-            s += buf;
-            // arrivals of the predecessors (ready_time, :67-78)
-            std::vector<std::string> xs;
-            for (size_t k = 0; k < preds[i].size(); ++k) {
-                const int q = preds[i][k];
-                const EdgeRec &er = p.edges[p.nodes[i].e_begin + k];
-                const std::string endq = where[q] == -1
-                    ? "e" + std::to_string(q)
-                    : "E[" + std::to_string((long long)where[q] * T) + "]";
-                const std::string gq = where[q] == -1
-                    ? "d" + std::to_string(q) : "(int)g[" + std::to_string(q) + "]";
-                const std::string x = "x" + std::to_string(i) + "_" + std::to_string(k);
-                if (er.c == 0.0 && !std::signbit(er.c)) {
-                    // zero-byte output: end + 0.0 == end for end >= +0
-                    s += "    const double " + x + " = " + endq + ";\n";
-                } else {
-                    s += "    const double " + x + " = " + endq + " + dsel(" + gq + " == " +
-                         di + ", 0.0, " + lit(er.c) + ");\n";
-                }
-                xs.push_back(x);
-            }
-            // max over predecessors: a balanced tree (no NaN can occur, so
-            // max is associative and the result equals the reference's fold)
-            std::string r = "r" + std::to_string(i);
-            if (xs.empty()) {
-                s += "    const double " + r + " = 0.0;\n";
-            } else {
-                int lvl = 0;
-                while (xs.size() > 1) {
-                    std::vector<std::string> nx;
-                    for (size_t k = 0; k + 1 < xs.size(); k += 2) {
-                        const std::string m = "m" + std::to_string(i) + "_" +
-                                              std::to_string(lvl) + "_" + std::to_string(k);
-                        s += "    const double " + m + " = " + mx + "(" + xs[k] + ", " +
-                             xs[k + 1] + ");\n";
-                        nx.push_back(m);
-                    }
-                    if (xs.size() & 1) nx.push_back(xs.back());
-                    xs.swap(nx);
-                    ++lvl;
-                }
-                // pymax(0.0, x) == x for x >= +0
-                s += "    const double " + r + " = " + xs[0] + ";\n";
-            }
-            std::vector<std::string> av, du;
-            for (int k = 0; k < K; ++k) {
-                av.push_back("a" + std::to_string(k));
-                du.push_back(lit(p.dur[size_t(i) * K + k]));
-            }
-            const std::string si = "s" + std::to_string(i);
-            const std::string Ai = "A" + std::to_string(i);
-            if (o.avail_smem) {
-                s += "    double *" + Ai + " = A + " + di + " * " + std::to_string(T) + ";\n";
-                s += "    const double " + si + " = " + mx + "(" + r + ", *" + Ai + ");\n";
-            } else {
-                s += "    const double " + si + " = " + mx + "(" + r + ", " + sel(di, av) + ");\n";
-            }
-            std::string dsrc = sel(di, du);
-            if (o.dur_smem && dsrc != du[0])
-                dsrc = "dur[" + std::to_string(i * K) + " + " + di + "]";
-            const std::string ei = "e" + std::to_string(i);
-            s += "    const double " + ei + " = " + si + " + " + dsrc + ";\n";
-            std::snprintf(buf, sizeof buf,
-                          "    if (TRACE && valid) starts[cand * %d + %d] = %s;\n", V, i,
-                          si.c_str());
-            s += buf;
-            if (where[i] >= 0)
-                s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + ei + ";\n";
-            if (o.avail_smem) {
-                s += "    *" + Ai + " = " + ei + ";\n";
-            } else {
-                for (int k = 0; k < K; ++k) {
-                    const std::string a = "a" + std::to_string(k);
-                    s += "    " + a + " = dsel(" + di + " == " + std::to_string(k) + ", " +
-                         ei + ", " + a + ");\n";
-                }
-            }
-        }
-        s += "    double ms = 0.0;\n";
-        for (int k = 0; k < K; ++k)
-            s += o.avail_smem ? "    ms = pymax(ms, A[" + std::to_string(k * T) + "]);\n"
-                              : "    ms = pymax(ms, a" + std::to_string(k) + ");\n";
-        std::snprintf(buf, sizeof buf,
-                      "    const int st = gmax >= %d ? ST_GENE : ST_OK;\n"
-                      "    ms_out = st ? knan() : ms;\n    st_out = st;\n  }\n};\n", K);
-        s += buf;
-        s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
-             "  extern __shared__ __align__(16) hs_u8 smem[];\n"
-             "  JitBody<TRACE> body;\n"
-             "  body.ends = reinterpret_cast<double *>(smem + a.smem_ends);\n"
-             "  body.avail = reinterpret_cast<double *>(smem + a.smem_kstate);\n"
-             "  body.dur = reinterpret_cast<const double *>(smem + 16);\n"
-             "  body.starts = a.starts;\n";
-        if (o.dur_smem) {
-            std::snprintf(buf, sizeof buf,
-                          "  { const uint4 *src = reinterpret_cast<const uint4 *>(a.blob + "
-                          "a.lay.dur);\n    uint4 *dst = reinterpret_cast<uint4 *>(smem + 16);\n"
-                          "    for (int q = threadIdx.x; q < %lld; q += blockDim.x) dst[q] = "
-                          "src[q]; }\n", (long long)(dur_bytes(p) / 16));
-            s += buf;
-        }
-        s += "  eval_tiles(a, smem, body);\n}\n";
-        std::snprintf(buf, sizeof buf,
-                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
-                      "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
-                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
-                      "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n", T, T);
-        s += buf;
-        return next;
     }
+    if (src == nullptr) return next;
+    const int ld_cap = p.pref_ld() + 16;
+    const JitLayout l = jit_layout(p, o, T, next, ld_cap);
+    const bool checks = p.mem_check || !p.all_batch_ok || !p.latency_complete || l.cls;
+    const std::string mx = o.int_max ? "pymax_nn" : "pymax";
+    std::string &s = *src;
+    s.clear();
+    char buf[1024];
+    s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
+    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, "
+         "const hs_u8 *g, int li, hs_i64 cand, bool valid, double *starts, double &ms_out, "
+         "int &st_out) {\n";
+    s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
+         ") + li;\n    (void)E;\n";
+    if (l.dur)
+        s += "    const double *DUR = reinterpret_cast<const double *>(smem + " +
+             std::to_string(l.dur_off) + ");\n";
+    if (l.cls) {
+        s += "    const double *CT = reinterpret_cast<const double *>(smem + " +
+             std::to_string(l.ctab_off) + ");\n";
+        s += "    const hs_u16 *BCL = reinterpret_cast<const hs_u16 *>(smem + " +
+             std::to_string(l.bcl_off) + ");\n";
+    }
+    if (l.avail) {
+        s += "    const hs_u32 A = smem_addr(smem + " + std::to_string(l.avail_off) +
+             ") + li * 8;\n";
+        for (int k = 0; k < K; ++k)
+            s += "    st_shared_f64(A + " + std::to_string(k * T * 8) + ", 0.0);\n";
+    } else {
+        for (int k = 0; k < K; ++k) s += "    double a" + std::to_string(k) + " = 0.0;\n";
+    }
+    if (l.mem) {
+        s += "    const double *CAP = reinterpret_cast<const double *>(smem + " +
+             std::to_string(l.cap_off) + ");\n";
+        s += "    const hs_u32 M = smem_addr(smem + " + std::to_string(l.mem_off) +
+             ") + li * 8;\n";
+        for (int k = 0; k < K; ++k)
+            s += "    st_shared_f64(M + " + std::to_string(k * T * 8) + ", 0.0);\n";
+    }
+    s += "    int gmax = 0;\n    int st = 0;\n";
+    uint64_t okmask = 0;
+    for (int k = 0; k < K; ++k)
+        if (p.okL[k]) okmask |= 1ull << k;
+    for (int i = 0; i < V; ++i) {
+        const std::string is = std::to_string(i);
+        const std::string di = "d" + is;
+        s += "    // " + p.task_ids[p.order[i]] + "\n";
+        // raw gene for the range check; clamped for table / state indexing
+        // (lanes past the last row read stale tile bytes)
+        std::snprintf(buf, sizeof buf,
+                      "    const int g%d = g[%d]; gmax = max(gmax, g%d);\n"
+                      "    const int %s = min(g%d, %d);\n", i, i, i, di.c_str(), i, K - 1);
+        s += buf;
+        // try_place order (heuristics.py:92-106): batch size, memory, links,
+        // latency entry; the first failing check decides the status
+        if (!p.all_batch_ok) {
+            std::snprintf(buf, sizeof buf,
+                          "    st = first_status(st, !((0x%llxull >> %s) & 1ull), ST_BATCH);\n",
+                          (unsigned long long)okmask, di.c_str());
+            s += buf;
+        }
+        if (l.mem) {
+            s += "    const hs_u32 M" + is + " = M + " + di + " * " + std::to_string(T * 8) +
+                 ";\n";
+            s += "    const double m" + is + " = ld_shared_f64(M" + is + ");\n";
+            s += "    st = first_status(st, m" + is + " + " + lit(p.extra[i]) + " > CAP[" +
+                 di + "], ST_MEMORY);\n";
+        }
+        std::vector<std::string> xs;
+        if (l.cls) s += "    int nl" + is + " = 0;\n";
+        for (size_t k = 0; k < preds[i].size(); ++k) {
+            const int q = preds[i][k];
+            const EdgeRec &er = p.edges[p.nodes[i].e_begin + k];
+            const std::string endq = where[q] == -1
+                ? "e" + std::to_string(q)
+                : "E[" + std::to_string((long long)where[q] * T) + "]";
+            const std::string gq = where[q] == -1
+                ? "d" + std::to_string(q)
+                : "min((int)g[" + std::to_string(q) + "], " + std::to_string(K - 1) + ")";
+            const std::string x = "x" + is + "_" + std::to_string(k);
+            if (l.cls) {
+                // comm class of (producer device, consumer device); 0xFFFF =
+                // missing link (core.py:153-154), class 0 = same device
+                const std::string c = "c" + is + "_" + std::to_string(k);
+                s += "    const int " + c + "r = BCL[" + gq + " * " + std::to_string(K) + " + " +
+                     di + "];\n";
+                s += "    nl" + is + " |= " + c + "r == 0xFFFF;\n";
+                s += "    const int " + c + " = min(" + c + "r, " + std::to_string(p.n_cls - 1) +
+                     ");\n";
+                s += "    const double " + x + " = " + endq + " + CT[" +
+                     std::to_string((long long)q * p.n_cls) + " + " + c + "];\n";
+            } else if (er.c == 0.0 && !std::signbit(er.c)) {
+                // zero-byte output: end + 0.0 == end for end >= +0
+                s += "    const double " + x + " = " + endq + ";\n";
+            } else {
+                s += "    const double " + x + " = " + endq + " + dsel(" + gq + " == " + di +
+                     ", 0.0, " + lit(er.c) + ");\n";
+            }
+            xs.push_back(x);
+        }
+        if (l.cls) s += "    st = first_status(st, nl" + is + ", ST_LINK);\n";
+        if (!p.latency_complete) {
+            uint64_t miss = 0;
+            for (int k = 0; k < K; ++k)
+                if (p.okL[k] && !p.dur_ok[size_t(i) * K + k]) miss |= 1ull << k;
+            if (miss) {
+                std::snprintf(buf, sizeof buf,
+                              "    st = first_status(st, (0x%llxull >> %s) & 1ull, ST_MISSING);\n",
+                              (unsigned long long)miss, di.c_str());
+                s += buf;
+            }
+        }
+        // max over predecessors: a balanced tree (no NaN can occur, so max
+        // is associative and the result equals the reference's fold)
+        const std::string r = "r" + is;
+        if (xs.empty()) {
+            s += "    const double " + r + " = 0.0;\n";
+        } else {
+            int lvl = 0;
+            while (xs.size() > 1) {
+                std::vector<std::string> nx;
+                for (size_t k = 0; k + 1 < xs.size(); k += 2) {
+                    const std::string m = "m" + is + "_" + std::to_string(lvl) + "_" +
+                                          std::to_string(k);
+                    s += "    const double " + m + " = " + mx + "(" + xs[k] + ", " +
+                         xs[k + 1] + ");\n";
+                    nx.push_back(m);
+                }
+                if (xs.size() & 1) nx.push_back(xs.back());
+                xs.swap(nx);
+                ++lvl;
+            }
+            s += "    const double " + r + " = " + xs[0] + ";\n";  // max(0.0, x) == x
+        }
+        std::vector<std::string> av, du;
+        for (int k = 0; k < K; ++k) {
+            av.push_back("a" + std::to_string(k));
+            du.push_back(lit(p.dur[size_t(i) * K + k]));
+        }
+        const std::string si = "s" + is, ei = "e" + is, Ai = "A" + is;
+        if (l.avail) {
+            s += "    const hs_u32 " + Ai + " = A + " + di + " * " + std::to_string(T * 8) +
+                 ";\n";
+            s += "    const double " + si + " = " + mx + "(" + r + ", ld_shared_f64(" + Ai +
+                 "));\n";
+        } else {
+            s += "    const double " + si + " = " + mx + "(" + r + ", " + sel(di, av) + ");\n";
+        }
+        std::string dsrc = l.dur ? "DUR[" + std::to_string(i * K) + " + " + di + "]" : sel(di, du);
+        if (l.dur) {
+            bool same = true;
+            for (auto &v : du) same = same && v == du[0];
+            if (same) dsrc = du[0];
+        }
+        s += "    const double " + ei + " = " + si + " + " + dsrc + ";\n";
+        std::snprintf(buf, sizeof buf,
+                      "    if (TRACE && valid) starts[cand * %d + %d] = %s;\n", V, i, si.c_str());
+        s += buf;
+        if (where[i] >= 0)
+            s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + ei + ";\n";
+        if (l.avail) {
+            s += "    st_shared_f64(" + Ai + ", " + ei + ");\n";
+        } else {
+            for (int k = 0; k < K; ++k) {
+                const std::string a = "a" + std::to_string(k);
+                s += "    " + a + " = dsel(" + di + " == " + std::to_string(k) + ", " + ei +
+                     ", " + a + ");\n";
+            }
+        }
+        if (l.mem)
+            s += "    st_shared_f64(M" + is + ", m" + is + " + " + lit(p.extra[i]) + ");\n";
+    }
+    s += "    double ms = 0.0;\n";
+    for (int k = 0; k < K; ++k)
+        s += l.avail ? "    ms = pymax(ms, ld_shared_f64(A + " + std::to_string(k * T * 8) +
+                           "));\n"
+                     : "    ms = pymax(ms, a" + std::to_string(k) + ");\n";
+    std::snprintf(buf, sizeof buf,
+                  "    if (gmax >= %d) st = ST_GENE;\n"
+                  "    ms_out = st ? (st >= ST_MISSING ? knan() : kinf()) : ms;\n"
+                  "    st_out = st;\n}\n", K);
+    s += buf;
+    (void)checks;
+    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts;\n"
+         "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
+         "bool valid, double &ms, int &st) {\n"
+         "    jit_body<TRACE>(smem, g, li, cand, valid, starts, ms, st);\n  }\n};\n";
+    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
+         "  extern __shared__ __align__(16) hs_u8 smem[];\n";
+    if (l.dur) s += stage(l.dur_off, "dur", int64_t(V) * K * 8);
+    if (l.cls) {
+        s += stage(l.ctab_off, "ctab", int64_t(V) * p.n_cls * 8);
+        s += stage(l.bcl_off, "bclass", int64_t(K) * K * 2);
+    }
+    if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
+    s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
+         "  eval_tiles(a, smem, body);\n}\n";
+    std::snprintf(buf, sizeof buf,
+                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
+                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n", T, T);
+    s += buf;
+    return next;
 }
 
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
@@ -331,8 +445,8 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     const JitOpts o = JitOpts::from_env();
     const int slots = jit_emit(p, 32, o, nullptr);
     const int ld_cap = p.pref_ld() + 16;
-    const int64_t per_lane = ld_cap + int64_t(slots) * 8 + (o.avail_smem ? 8 * p.K : 0);
-    const int64_t head = 16 + (o.dur_smem ? dur_bytes(p) : 0);
+    const int64_t per_lane = per_lane_bytes(p, o, slots, ld_cap);
+    const int64_t head = head_bytes(p, o);
     const int64_t budget = int64_t(optin) - head - 1024;
     int T = int(std::min<int64_t>(budget / per_lane, 256) / 32 * 32);
     if (T < 32) {
@@ -372,10 +486,13 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->slots = slots;
     m->ld_cap = ld_cap;
     m->opts = o;
-    m->smem_tile = head;
-    m->smem_ends = head + ((int64_t(T) * ld_cap + 15) & ~int64_t(15));
-    m->smem_kstate = m->smem_ends + int64_t(slots) * T * 8;
-    m->smem = size_t(m->smem_kstate + (o.avail_smem ? int64_t(8) * p.K * T : 0));
+    {
+        const JitLayout l = jit_layout(p, o, T, slots, ld_cap);
+        m->smem_tile = l.tile;
+        m->smem_ends = l.ends;
+        m->smem_kstate = l.avail_off;
+        m->smem = size_t(l.total);
+    }
     cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0,
                                         nullptr, nullptr, 0);
     if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern, m->lib, "hs_jit_eval");
