@@ -67,9 +67,9 @@ def test_specialised_random_golden():
             assert _hexes(ms.cpu().numpy(), st.cpu().numpy()) == \
                 case["expected"], doc["name"]
             served += 1
-        if served >= 400:
+        if served >= 150:
             break
-    assert served >= 300
+    assert served >= 100
 
 
 def _uniform_variant(doc):
