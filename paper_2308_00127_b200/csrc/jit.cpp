@@ -113,6 +113,7 @@ JitOpts JitOpts::from_env() {
             if (k == "avail") o.avail_smem = v == "smem";
             if (k == "dur") o.dur_smem = v == "smem";
             if (k == "max") o.int_max = v == "int";
+            if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
     }
@@ -448,7 +449,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     const int64_t per_lane = per_lane_bytes(p, o, slots, ld_cap);
     const int64_t head = head_bytes(p, o);
     const int64_t budget = int64_t(optin) - head - 1024;
-    int T = int(std::min<int64_t>(budget / per_lane, 256) / 32 * 32);
+    int T = int(std::min<int64_t>(budget / per_lane, o.lanes) / 32 * 32);
     if (T < 32) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;

@@ -18,6 +18,7 @@ struct JitOpts {
     bool avail_smem = true;   // per-device available times in shared memory
     bool dur_smem = true;     // latency table in shared memory (else selects)
     bool int_max = false;     // max via int64 compare of bit patterns
+    int lanes = 256;          // threads (= candidates) per CTA, at most
     static JitOpts from_env();
 };
 

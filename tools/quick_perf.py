@@ -22,7 +22,7 @@ for name in sys.argv[1:] or ["ws200"]:
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    reps = 5
+    reps = 10
     for _ in range(reps):
         plan.eval(genes, ms, None, best)
     e1.record(); torch.cuda.synchronize()
