@@ -203,9 +203,11 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
                                   "evaluator (live end-time slots of one warp "
                                   "exceed the per-CTA shared memory)");
 
+    const hs::JitModule *jm = p.batched ? nullptr : hs::find_jit(p, ds->device);
     Scratch repack;
     repack.s = stream;
-    if (!gen && !packed && n > 0 && ld > ds->ld_cap) {
+    // the specialised kernel reads its staged rows as 32-bit words
+    if (!gen && !packed && n > 0 && (ld > ds->ld_cap || (jm && ld % 4))) {
         // exotic row stride: compact to the preferred stride first
         const int64_t pl = p.pref_ld();
         CK(cudaMallocAsync(&repack.ptr, size_t(n * pl), stream));
@@ -215,7 +217,6 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
         genes = static_cast<const uint8_t *>(repack.ptr);
         ld = pl;
     }
-    const hs::JitModule *jm = p.batched ? nullptr : hs::find_jit(p, ds->device);
     const int lanes = jm ? jm->lanes : ds->lanes;
     const int64_t ntiles = (n + lanes - 1) / lanes;
     const int64_t cap = jm ? int64_t(jm->sms) * jm->blocks_per_sm
@@ -264,6 +265,13 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     a.best = reinterpret_cast<hsk::Best *>(best);
     a.index_base = index_base;
     a.smem_tile = jm ? jm->smem_tile : ds->smem_tile;
+    if (jm) {
+        a.sanitize = 1;
+        // double-buffered TMA staging when every tile is one bulk copy
+        const int64_t tail = n % lanes;
+        if (!gen && !packed && a.bulk && (tail * ld) % 16 == 0 && n > 0)
+            a.smem_tile2 = jm->smem_tile2;
+    }
     a.smem_ends = jm ? jm->smem_ends : ds->smem_ends;
     a.smem_kstate = jm ? jm->smem_kstate : ds->smem_kstate;
     if (jm) {

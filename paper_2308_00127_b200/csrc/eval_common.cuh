@@ -91,6 +91,8 @@ struct EvalParams {
     Best *partial;      // [grid]
     hs_u32 *ticket;
     hs_i64 index_base;
+    hs_i64 smem_tile2;  // second genome tile (double buffering), 0 = none
+    int sanitize;       // clamp staged genes to < gene_range, flag overflows
     hs_i64 smem_tile;   // byte offsets in shared memory: genome tile,
     hs_i64 smem_ends;   // [slot][lane] end times,
     hs_i64 smem_kstate; // [2K][lane] device state (generic K)
@@ -296,81 +298,135 @@ __device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 c
     }
 }
 
-// The CTA tile loop. `body.run(row, lane, cand, valid, ms, st)` evaluates
-// the lane's candidate from its staged genome row.
+// Issue the TMA bulk copy of a tile's genome rows (one elected thread).
+__device__ __forceinline__ void issue_tile(const EvalParams &a, hs_i64 tile, hs_u8 *dst,
+                                           hs_u64 *bar) {
+    const hs_i64 c0 = tile * a.lanes;
+    const hs_i64 left = a.n - c0;
+    const hs_i64 rows = left < a.lanes ? left : a.lanes;
+    bulk_g2s(dst, a.genes + c0 * a.ld, (hs_u32)(rows * a.ld), bar);
+}
+
+// The CTA tile loop. `body.run(row, lane, cand, valid, gene_bad, ms, st)`
+// evaluates the lane's candidate from its staged genome row; `gene_bad` is
+// set when the row was sanitised (a.sanitize) and held a gene >= K.
 template <class Body>
 __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Body &body) {
-    hs_u64 *bar = reinterpret_cast<hs_u64 *>(smem);
+    hs_u64 *bar = reinterpret_cast<hs_u64 *>(smem);  // two mbarriers
     hs_u8 *gtile = smem + a.smem_tile;
+    // double-buffered TMA staging: tile t+grid streams in while t computes
+    const bool dbuf = a.smem_tile2 != 0;
     const int T = blockDim.x, tid = threadIdx.x;
     const int lanes = a.lanes;
-    if (tid == 0) mbar_init(bar);
+    if (tid == 0) {
+        mbar_init(bar);
+        mbar_init(bar + 1);
+    }
     __syncthreads();
     double bc = kinf();
     hs_i64 bi = 0x7fffffffffffffffll;
-    hs_u32 phase = 0;
+    hs_u32 phase0 = 0, phase1 = 0;
     const hs_i64 ntiles = (a.n + lanes - 1) / lanes;
-    for (hs_i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (dbuf && tid == 0 && (hs_i64)blockIdx.x < ntiles)
+        issue_tile(a, blockIdx.x, gtile, bar);
+    int it = 0;
+    for (hs_i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const hs_i64 c0 = tile * lanes;
         const hs_i64 left = a.n - c0;
         const int rows = left < lanes ? (int)left : lanes;
-        __syncthreads();  // the previous tile's genomes are no longer read
-        if (a.gen) {
-            if (tid < rows) {
-                hs_u8 *r8 = gtile + (hs_i64)tid * a.ld_s;
-                gen_row(a, r8, a.first + c0 + tid);
-                if (a.genes_out) {
-                    hs_u8 *o = a.genes_out + (c0 + tid) * (hs_i64)a.V;
-                    for (int i = 0; i < a.V; ++i) o[i] = r8[i];
-                }
-            }
-        } else {
-            const hs_i64 bytes = (hs_i64)rows * a.ld;
-            const hs_u8 *src = a.genes + c0 * a.ld;
-            // packed rows land in the last bytes of the tile and are
-            // expanded in place (all rows read before any row is written)
-            hs_u8 *dst = a.packed ? gtile + (hs_i64)lanes * a.ld_s - (hs_i64)lanes * a.ld
-                                  : gtile;
-            if (a.bulk && bytes > 0 && (bytes & 15) == 0) {
-                if (tid == 0) bulk_g2s(dst, src, (hs_u32)bytes, bar);
-                mbar_wait(bar, phase);
-                phase ^= 1u;
+        hs_u8 *cur = gtile;
+        if (dbuf) {
+            const int b = it & 1;
+            cur = b ? smem + a.smem_tile2 : gtile;
+            if (b) {
+                mbar_wait(bar + 1, phase1);
+                phase1 ^= 1u;
             } else {
-                for (hs_i64 b = tid; b < bytes; b += T) dst[b] = src[b];
+                mbar_wait(bar, phase0);
+                phase0 ^= 1u;
             }
-            if (a.packed) {
-                __syncthreads();
-                // 2-bit genes, 16 per word: word w -> four 4-gene words
-                hs_u32 pk[64];
-                const int nw = (int)(a.ld >> 2);
-                const hs_u32 *prow = reinterpret_cast<const hs_u32 *>(dst + (hs_i64)tid * a.ld);
+            __syncthreads();  // every lane is done with the other buffer
+            if (tid == 0 && tile + gridDim.x < ntiles)
+                issue_tile(a, tile + gridDim.x, b ? gtile : smem + a.smem_tile2,
+                           b ? bar : bar + 1);
+        } else {
+            __syncthreads();  // the previous tile's genomes are no longer read
+            if (a.gen) {
+                if (tid < rows) {
+                    hs_u8 *r8 = gtile + (hs_i64)tid * a.ld_s;
+                    gen_row(a, r8, a.first + c0 + tid);
+                    if (a.genes_out) {
+                        hs_u8 *o = a.genes_out + (c0 + tid) * (hs_i64)a.V;
+                        for (int i = 0; i < a.V; ++i) o[i] = r8[i];
+                    }
+                }
+            } else {
+                const hs_i64 bytes = (hs_i64)rows * a.ld;
+                const hs_u8 *src = a.genes + c0 * a.ld;
+                // packed rows land in the last bytes of the tile and are
+                // expanded in place (all rows read before any row is written)
+                hs_u8 *dst = a.packed ? gtile + (hs_i64)lanes * a.ld_s - (hs_i64)lanes * a.ld
+                                      : gtile;
+                if (a.bulk && bytes > 0 && (bytes & 15) == 0) {
+                    if (tid == 0) bulk_g2s(dst, src, (hs_u32)bytes, bar);
+                    mbar_wait(bar, phase0);
+                    phase0 ^= 1u;
+                } else {
+                    for (hs_i64 b = tid; b < bytes; b += T) dst[b] = src[b];
+                }
+                if (a.packed) {
+                    __syncthreads();
+                    // 2-bit genes, 16 per word: word w -> four 4-gene words
+                    hs_u32 pk[64];
+                    const int nw = (int)(a.ld >> 2);
+                    const hs_u32 *prow =
+                        reinterpret_cast<const hs_u32 *>(dst + (hs_i64)tid * a.ld);
 #pragma unroll 4
-                for (int w = 0; w < nw && w < 64; ++w) pk[w] = tid < rows ? prow[w] : 0u;
-                __syncthreads();
-                hs_u32 *orow = reinterpret_cast<hs_u32 *>(gtile + (hs_i64)tid * a.ld_s);
-                const int nout = a.ld_s >> 2;
+                    for (int w = 0; w < nw && w < 64; ++w) pk[w] = tid < rows ? prow[w] : 0u;
+                    __syncthreads();
+                    hs_u32 *orow = reinterpret_cast<hs_u32 *>(gtile + (hs_i64)tid * a.ld_s);
+                    const int nout = a.ld_s >> 2;
 #pragma unroll 4
-                for (int w = 0; w < nw && w < 64; ++w) {
-                    const hs_u32 x = pk[w];
+                    for (int w = 0; w < nw && w < 64; ++w) {
+                        const hs_u32 x = pk[w];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int o = 4 * w + j;
-                        if (o < nout) {
-                            const hs_u32 b = (x >> (8 * j)) & 0xFFu;
-                            orow[o] = (b & 3u) | ((b & 0xCu) << 6) | ((b & 0x30u) << 12) |
-                                      ((b & 0xC0u) << 18);
+                        for (int j = 0; j < 4; ++j) {
+                            const int o = 4 * w + j;
+                            if (o < nout) {
+                                const hs_u32 b = (x >> (8 * j)) & 0xFFu;
+                                orow[o] = (b & 3u) | ((b & 0xCu) << 6) | ((b & 0x30u) << 12) |
+                                          ((b & 0xC0u) << 18);
+                            }
                         }
                     }
                 }
             }
+            __syncthreads();
         }
-        __syncthreads();
         const int li = tid;
         const hs_i64 cand = c0 + li;
         const bool valid = li < rows;
+        hs_u8 *row = cur + (hs_i64)li * a.ld_s;
+        int gene_bad = 0;
+        if (a.sanitize) {
+            // one pass over the lane's own row: flag genes >= K, clamp every
+            // byte to K-1 so the specialised code can index by gene freely
+            // (rows past the last candidate hold stale bytes)
+            hs_u32 *w = reinterpret_cast<hs_u32 *>(row);
+            const int nw = (a.V + 3) >> 2;
+            const hs_u32 kmax = (hs_u32)(a.gene_range - 1) * 0x01010101u;
+            const int tail = a.V & 3;
+            for (int j = 0; j < nw; ++j) {
+                const hs_u32 x = w[j];
+                hs_u32 over = __vcmpgtu4(x, kmax);
+                if (j == nw - 1 && tail) over &= (1u << (8 * tail)) - 1u;
+                gene_bad |= over != 0u;
+                w[j] = __vminu4(x, kmax);
+            }
+        }
         double ms;
         int st;
-        body.run(gtile + (hs_i64)li * a.ld_s, li, cand, valid, ms, st);
+        body.run(row, li, cand, valid, gene_bad, ms, st);
         if (valid) {
             if (a.makespan) a.makespan[cand] = ms;
             if (a.status) a.status[cand] = (hs_u8)st;

@@ -138,7 +138,7 @@ namespace {
 struct JitLayout {
     bool dur = false, cls = false, mem = false, avail = false;
     int64_t dur_off = 0, ctab_off = 0, bcl_off = 0, cap_off = 0, head = 16;
-    int64_t tile = 0, ends = 0, avail_off = 0, mem_off = 0, total = 0;
+    int64_t tile = 0, tile2 = 0, ends = 0, avail_off = 0, mem_off = 0, total = 0;
 };
 
 JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap) {
@@ -156,7 +156,8 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
     if (l.mem) { l.cap_off = at; at += a16(int64_t(p.K) * 8); }
     l.head = at;
     l.tile = at;
-    l.ends = l.tile + a16(int64_t(T) * ld_cap);
+    l.tile2 = l.tile + a16(int64_t(T) * ld_cap);
+    l.ends = l.tile2 + a16(int64_t(T) * ld_cap);
     at = l.ends + int64_t(slots) * T * 8;
     if (l.avail) { l.avail_off = at; at += int64_t(p.K) * T * 8; }
     if (l.mem) { l.mem_off = at; at += int64_t(p.K) * T * 8; }
@@ -166,7 +167,7 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
 
 int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap) {
     const bool avail = o.avail_smem || p.K > 4;
-    return ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
+    return 2 * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
 }
 
 int64_t head_bytes(const Plan &p, const JitOpts &o) {
@@ -233,8 +234,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     char buf[1024];
     s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, "
-         "const hs_u8 *g, int li, hs_i64 cand, bool valid, double *starts, double &ms_out, "
-         "int &st_out) {\n";
+         "const hs_u8 *g, int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
+         "double &ms_out, int &st_out) {\n";
     s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
          ") + li;\n    (void)E;\n";
     if (l.dur)
@@ -262,7 +263,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int k = 0; k < K; ++k)
             s += "    st_shared_f64(M + " + std::to_string(k * T * 8) + ", 0.0);\n";
     }
-    s += "    int gmax = 0;\n    int st = 0;\n";
+    s += "    int st = 0;\n";
     uint64_t okmask = 0;
     for (int k = 0; k < K; ++k)
         if (p.okL[k]) okmask |= 1ull << k;
@@ -272,10 +273,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         s += "    // " + p.task_ids[p.order[i]] + "\n";
         // raw gene for the range check; clamped for table / state indexing
         // (lanes past the last row read stale tile bytes)
-        std::snprintf(buf, sizeof buf,
-                      "    const int g%d = g[%d]; gmax = max(gmax, g%d);\n"
-                      "    const int %s = min(g%d, %d);\n", i, i, i, di.c_str(), i, K - 1);
-        s += buf;
+        // genes were range-checked and clamped when the row was staged
+        s += "    const int " + di + " = g[" + is + "];\n";
         // try_place order (heuristics.py:92-106): batch size, memory, links,
         // latency entry; the first failing check decides the status
         if (!p.all_batch_ok) {
@@ -301,7 +300,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 : "E[" + std::to_string((long long)where[q] * T) + "]";
             const std::string gq = where[q] == -1
                 ? "d" + std::to_string(q)
-                : "min((int)g[" + std::to_string(q) + "], " + std::to_string(K - 1) + ")";
+                : "(int)g[" + std::to_string(q) + "]";
             const std::string x = "x" + is + "_" + std::to_string(k);
             if (l.cls) {
                 // comm class of (producer device, consumer device); 0xFFFF =
@@ -401,15 +400,15 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                            "));\n"
                      : "    ms = pymax(ms, a" + std::to_string(k) + ");\n";
     std::snprintf(buf, sizeof buf,
-                  "    if (gmax >= %d) st = ST_GENE;\n"
+                  "    if (gene_bad) st = ST_GENE;\n"
                   "    ms_out = st ? (st >= ST_MISSING ? knan() : kinf()) : ms;\n"
-                  "    st_out = st;\n}\n", K);
+                  "    st_out = st;\n}\n");
     s += buf;
     (void)checks;
     s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
-         "bool valid, double &ms, int &st) {\n"
-         "    jit_body<TRACE>(smem, g, li, cand, valid, starts, ms, st);\n  }\n};\n";
+         "bool valid, int gene_bad, double &ms, int &st) {\n"
+         "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st);\n  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
          "  extern __shared__ __align__(16) hs_u8 smem[];\n";
     if (l.dur) s += stage(l.dur_off, "dur", int64_t(V) * K * 8);
@@ -490,6 +489,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     {
         const JitLayout l = jit_layout(p, o, T, slots, ld_cap);
         m->smem_tile = l.tile;
+        m->smem_tile2 = l.tile2;
         m->smem_ends = l.ends;
         m->smem_kstate = l.avail_off;
         m->smem = size_t(l.total);

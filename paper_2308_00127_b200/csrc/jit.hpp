@@ -28,7 +28,7 @@ struct JitModule {
     cudaKernel_t kern = nullptr, kern_trace = nullptr;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;
-    int64_t smem_tile = 0, smem_ends = 0, smem_kstate = 0;
+    int64_t smem_tile = 0, smem_tile2 = 0, smem_ends = 0, smem_kstate = 0;
     JitOpts opts;
     size_t src_bytes = 0;
     double compile_ms = 0.0;

@@ -92,7 +92,7 @@ struct PlanBody {
     hs_u32 flags;
 
     __device__ __forceinline__ void run(const hs_u8 *grow, int li, hs_i64 cand,
-                                        bool valid, double &ms_out, int &st_out) {
+                                        bool valid, int, double &ms_out, int &st_out) {
         double *ecol = ends + li;
         typename DevStateSel<KT>::type avail, mem;
         if constexpr (KT == 0) {
@@ -189,7 +189,7 @@ struct BatchedBody {
     bool nan;
 
     __device__ __forceinline__ void run(const hs_u8 *grow, int li, hs_i64 cand,
-                                        bool valid, double &ms_out, int &st_out) {
+                                        bool valid, int, double &ms_out, int &st_out) {
         double *ecol = ends + li;
         double *av = kstate + li;
         for (int k = 0; k < K; ++k) av[k * lanes] = 0.0;
