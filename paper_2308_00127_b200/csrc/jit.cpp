@@ -136,13 +136,15 @@ namespace {
 // Shared-memory layout of the specialised kernel (byte offsets); every
 // table is staged from the plan blob once per CTA.
 struct JitLayout {
-    bool dur = false, cls = false, mem = false, avail = false;
+    bool dur = false, cls = false, mem = false, avail = false, dbuf = true;
     int64_t dur_off = 0, ctab_off = 0, bcl_off = 0, cap_off = 0, head = 16;
     int64_t tile = 0, tile2 = 0, ends = 0, avail_off = 0, mem_off = 0, total = 0;
 };
 
-JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap) {
+JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap,
+                     bool dbuf = true) {
     JitLayout l;
+    l.dbuf = dbuf;
     l.dur = o.dur_smem || p.K > 4;
     l.avail = o.avail_smem || p.K > 4;
     l.cls = !p.uniform_comm;
@@ -156,8 +158,8 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
     if (l.mem) { l.cap_off = at; at += a16(int64_t(p.K) * 8); }
     l.head = at;
     l.tile = at;
-    l.tile2 = l.tile + a16(int64_t(T) * ld_cap);
-    l.ends = l.tile2 + a16(int64_t(T) * ld_cap);
+    l.tile2 = dbuf ? l.tile + a16(int64_t(T) * ld_cap) : 0;
+    l.ends = l.tile + a16(int64_t(T) * ld_cap) * (dbuf ? 2 : 1);
     at = l.ends + int64_t(slots) * T * 8;
     if (l.avail) { l.avail_off = at; at += int64_t(p.K) * T * 8; }
     if (l.mem) { l.mem_off = at; at += int64_t(p.K) * T * 8; }
@@ -165,9 +167,10 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
     return l;
 }
 
-int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap) {
+int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap,
+                       bool dbuf) {
     const bool avail = o.avail_smem || p.K > 4;
-    return 2 * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
+    return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
 }
 
 int64_t head_bytes(const Plan &p, const JitOpts &o) {
@@ -226,7 +229,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     }
     if (src == nullptr) return next;
     const int ld_cap = p.pref_ld() + 16;
-    const JitLayout l = jit_layout(p, o, T, next, ld_cap);
+    const JitLayout l = jit_layout(p, o, T, next, ld_cap, o.dbuf);
     const bool checks = p.mem_check || !p.all_batch_ok || !p.latency_complete || l.cls;
     const std::string mx = o.int_max ? "pymax_nn" : "pymax";
     std::string &s = *src;
@@ -445,16 +448,23 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     const JitOpts o = JitOpts::from_env();
     const int slots = jit_emit(p, 32, o, nullptr);
     const int ld_cap = p.pref_ld() + 16;
-    const int64_t per_lane = per_lane_bytes(p, o, slots, ld_cap);
     const int64_t head = head_bytes(p, o);
     const int64_t budget = int64_t(optin) - head - 1024;
-    int T = int(std::min<int64_t>(budget / per_lane, o.lanes) / 32 * 32);
+    auto lanes_for = [&](bool db) {
+        return int(std::min<int64_t>(budget / per_lane_bytes(p, o, slots, ld_cap, db),
+                                     o.lanes) / 32 * 32);
+    };
+    // double-buffer the genome tile only when it costs no lanes
+    const bool dbuf = lanes_for(true) >= lanes_for(false);
+    int T = lanes_for(dbuf);
     if (T < 32) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
     }
     std::string src;
-    jit_emit(p, T, o, &src);
+    JitOpts oe = o;
+    oe.dbuf = dbuf;
+    jit_emit(p, T, oe, &src);
     const char *hdr_src[] = {kEvalCommonSrc};
     const char *hdr_name[] = {"eval_common.cuh"};
     nvrtcProgram_t prog = nullptr;
@@ -487,7 +497,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->ld_cap = ld_cap;
     m->opts = o;
     {
-        const JitLayout l = jit_layout(p, o, T, slots, ld_cap);
+        const JitLayout l = jit_layout(p, o, T, slots, ld_cap, dbuf);
         m->smem_tile = l.tile;
         m->smem_tile2 = l.tile2;
         m->smem_ends = l.ends;

@@ -19,6 +19,7 @@ struct JitOpts {
     bool dur_smem = true;     // latency table in shared memory (else selects)
     bool int_max = false;     // max via int64 compare of bit patterns
     int lanes = 256;          // threads (= candidates) per CTA, at most
+    bool dbuf = true;         // (set by jit_build) double-buffered genome tile
     static JitOpts from_env();
 };
 
