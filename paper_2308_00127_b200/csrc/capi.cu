@@ -219,7 +219,11 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     }
     const int lanes = jm ? jm->lanes : ds->lanes;
     const int64_t ntiles = (n + lanes - 1) / lanes;
-    const int64_t cap = jm ? int64_t(jm->sms) * jm->blocks_per_sm
+    // the direct-load kernel (jit_direct_ok) packs several CTAs per SM
+    const bool direct = jm && jm->kern_direct && !starts && !gen && !packed && ld % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(genes) & 3) == 0;
+    const int64_t cap = jm ? int64_t(jm->sms) *
+                                 (direct ? jm->blocks_per_sm_direct : jm->blocks_per_sm)
                            : int64_t(ds->sms) * ds->blocks_per_sm;
     const int grid = int(std::max<int64_t>(1, std::min(ntiles, cap)));
 

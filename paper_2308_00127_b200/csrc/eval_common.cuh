@@ -113,6 +113,15 @@ __device__ __forceinline__ double pymax_nn(double a, double b) {
     return __double_as_longlong(b) > __double_as_longlong(a) ? b : a;
 }
 
+// four genes (bytes <= 3) -> 8 bits, byte b at bits 2b..2b+1
+__device__ __forceinline__ hs_u32 pack4(hs_u32 w) {
+    const hs_u32 x = w | (w >> 6);
+    return (x | (x >> 12)) & 0xFFu;
+}
+__device__ __forceinline__ hs_u32 pack16(hs_u32 a, hs_u32 b, hs_u32 c, hs_u32 d) {
+    return pack4(a) | (pack4(b) << 8) | (pack4(c) << 16) | (pack4(d) << 24);
+}
+
 // branch-free select (kept as FSEL pairs: the specialised code relies on it
 // to stay divergence free when lanes map tasks to different devices)
 __device__ __forceinline__ double dsel(bool p, double a, double b) {

@@ -113,6 +113,10 @@ JitOpts JitOpts::from_env() {
             if (k == "avail") o.avail_smem = v == "smem";
             if (k == "dur") o.dur_smem = v == "smem";
             if (k == "max") o.int_max = v == "int";
+            if (k == "genes") o.genes_reg = v == "reg";
+            if (k == "near") o.near = std::atoi(v.c_str());
+            if (k == "ctas") o.ctas = std::max(1, std::atoi(v.c_str()));
+            if (k == "ahead") o.ahead = std::atoi(v.c_str());
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -157,12 +161,16 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
     }
     if (l.mem) { l.cap_off = at; at += a16(int64_t(p.K) * 8); }
     l.head = at;
-    l.tile = at;
-    l.tile2 = dbuf ? l.tile + a16(int64_t(T) * ld_cap) : 0;
-    l.ends = l.tile + a16(int64_t(T) * ld_cap) * (dbuf ? 2 : 1);
+    // per-lane state first, genome tiles last: the direct-load kernel
+    // (genes read from global memory into registers) needs only [0, tile)
+    l.ends = at;
     at = l.ends + int64_t(slots) * T * 8;
     if (l.avail) { l.avail_off = at; at += int64_t(p.K) * T * 8; }
     if (l.mem) { l.mem_off = at; at += int64_t(p.K) * T * 8; }
+    at = a16(at);
+    l.tile = at;
+    l.tile2 = dbuf ? l.tile + a16(int64_t(T) * ld_cap) : 0;
+    at = l.tile + a16(int64_t(T) * ld_cap) * (dbuf ? 2 : 1);
     l.total = at;
     return l;
 }
@@ -204,7 +212,53 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     // register residency for short-lived end times, slots for the rest
     std::vector<int> where(V, -2);  // -2 none, -1 register, >=0 slot
     int next = 0;
-    {
+    const int near = o.near;
+    if (near > 0) {
+        // split residency: every end time is a register value for the
+        // consumers within `near` positions; a value with farther consumers
+        // also gets long storage, a register when at most `reg_budget` such
+        // values overlap (greedy by end point = the maximum number of
+        // intervals), else a shared-memory slot (interval colouring)
+        std::vector<int> far_last(V, -1);
+        for (int i = 0; i < V; ++i)
+            for (int q : preds[i])
+                if (i - q > near) far_last[q] = std::max(far_last[q], i);
+        std::vector<int> byend;
+        for (int q = 0; q < V; ++q) {
+            if (last[q] < 0) continue;
+            if (far_last[q] < 0) where[q] = -1;
+            else byend.push_back(q);
+        }
+        std::sort(byend.begin(), byend.end(), [&](int a, int b) {
+            return far_last[a] != far_last[b] ? far_last[a] < far_last[b] : a < b;
+        });
+        std::vector<int> load(V + 1, 0);
+        std::vector<char> to_slot(V, 0);
+        for (int q : byend) {
+            int mx = 0;
+            for (int t = q; t < far_last[q]; ++t) mx = std::max(mx, load[t]);
+            if (mx < reg_budget) {
+                where[q] = -1;
+                for (int t = q; t < far_last[q]; ++t) ++load[t];
+            } else {
+                to_slot[q] = 1;
+            }
+        }
+        std::vector<std::vector<int>> dies(V);
+        for (int q = 0; q < V; ++q)
+            if (to_slot[q]) dies[far_last[q]].push_back(q);
+        std::priority_queue<int, std::vector<int>, std::greater<int>> freel;
+        for (int i = 0; i < V; ++i) {
+            for (int q : dies[i]) freel.push(where[q]);
+            if (!to_slot[i]) continue;
+            if (!freel.empty()) {
+                where[i] = freel.top();
+                freel.pop();
+            } else {
+                where[i] = next++;
+            }
+        }
+    } else {
         std::vector<std::vector<int>> dies(V);
         for (int i = 0; i < V; ++i)
             if (last[i] >= 0) dies[last[i]].push_back(i);
@@ -236,8 +290,11 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     s.clear();
     char buf[1024];
     s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
-    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, "
-         "const hs_u8 *g, int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
+    const bool greg = o.genes_reg && K <= 4;
+    const int NP = (V + 15) / 16, NW = (V + 3) / 4;
+    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
+         std::string(greg ? "const hs_u32 *GPA" : "const hs_u8 *g") +
+         ", int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
          "double &ms_out, int &st_out) {\n";
     s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
          ") + li;\n    (void)E;\n";
@@ -266,43 +323,54 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int k = 0; k < K; ++k)
             s += "    st_shared_f64(M + " + std::to_string(k * T * 8) + ", 0.0);\n";
     }
+    // genes 2 bits each in registers: no shared-memory gene loads on the
+    // per-task chain, and no aliasing between gene reads and slot stores
+    auto gexpr = [&](int q) {
+        const int j = q >> 4, sh = 2 * (q & 15);
+        std::string w = "GP" + std::to_string(j);
+        if (sh) w = "(" + w + " >> " + std::to_string(sh) + ")";
+        return sh == 30 ? "(int)" + w : "(int)(" + w + " & 3u)";
+    };
+    if (greg)
+        for (int j = 0; j < NP; ++j)
+            s += "    const hs_u32 GP" + std::to_string(j) + " = GPA[" + std::to_string(j) +
+                 "];\n";
     s += "    int st = 0;\n";
     uint64_t okmask = 0;
     for (int k = 0; k < K; ++k)
         if (p.okL[k]) okmask |= 1ull << k;
-    for (int i = 0; i < V; ++i) {
-        const std::string is = std::to_string(i);
-        const std::string di = "d" + is;
-        s += "    // " + p.task_ids[p.order[i]] + "\n";
-        // raw gene for the range check; clamped for table / state indexing
-        // (lanes past the last row read stale tile bytes)
-        // genes were range-checked and clamped when the row was staged
-        s += "    const int " + di + " = g[" + is + "];\n";
-        // try_place order (heuristics.py:92-106): batch size, memory, links,
-        // latency entry; the first failing check decides the status
-        if (!p.all_batch_ok) {
-            std::snprintf(buf, sizeof buf,
-                          "    st = first_status(st, !((0x%llxull >> %s) & 1ull), ST_BATCH);\n",
-                          (unsigned long long)okmask, di.c_str());
-            s += buf;
+    // max over a list of terms: a balanced tree (no NaN can occur, so max
+    // is associative and the result equals the reference's fold)
+    auto max_tree = [&](std::vector<std::string> xs, const std::string &tag) {
+        int lvl = 0;
+        while (xs.size() > 1) {
+            std::vector<std::string> nx;
+            for (size_t k = 0; k + 1 < xs.size(); k += 2) {
+                const std::string m = "m" + tag + "_" + std::to_string(lvl) + "_" +
+                                      std::to_string(k);
+                s += "    const double " + m + " = " + mx + "(" + xs[k] + ", " + xs[k + 1] +
+                     ");\n";
+                nx.push_back(m);
+            }
+            if (xs.size() & 1) nx.push_back(xs.back());
+            xs.swap(nx);
+            ++lvl;
         }
-        if (l.mem) {
-            s += "    const hs_u32 M" + is + " = M + " + di + " * " + std::to_string(T * 8) +
-                 ";\n";
-            s += "    const double m" + is + " = ld_shared_f64(M" + is + ");\n";
-            s += "    st = first_status(st, m" + is + " + " + lit(p.extra[i]) + " > CAP[" +
-                 di + "], ST_MEMORY);\n";
-        }
+        return xs[0];
+    };
+    // one relaxation term end(q) + comm(q -> i) per predecessor
+    auto edge_terms = [&](int i, int k0, int k1) {
+        const std::string is = std::to_string(i), di = "d" + is;
         std::vector<std::string> xs;
-        if (l.cls) s += "    int nl" + is + " = 0;\n";
-        for (size_t k = 0; k < preds[i].size(); ++k) {
+        for (int k = k0; k < k1; ++k) {
             const int q = preds[i][k];
             const EdgeRec &er = p.edges[p.nodes[i].e_begin + k];
-            const std::string endq = where[q] == -1
+            const bool in_reg = where[q] == -1 || (near > 0 && i - q <= near);
+            const std::string endq = in_reg
                 ? "e" + std::to_string(q)
                 : "E[" + std::to_string((long long)where[q] * T) + "]";
-            const std::string gq = where[q] == -1
-                ? "d" + std::to_string(q)
+            const std::string gq = greg ? gexpr(q)
+                : in_reg ? "d" + std::to_string(q)
                 : "(int)g[" + std::to_string(q) + "]";
             const std::string x = "x" + is + "_" + std::to_string(k);
             if (l.cls) {
@@ -319,12 +387,70 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             } else if (er.c == 0.0 && !std::signbit(er.c)) {
                 // zero-byte output: end + 0.0 == end for end >= +0
                 s += "    const double " + x + " = " + endq + ";\n";
+            } else if (greg) {
+                // same device <=> the 2-bit fields agree: one LOP3 per edge
+                const int j = q >> 4, sh = 2 * (q & 15);
+                char mk[32];
+                std::snprintf(mk, sizeof mk, "0x%xu", 3u << sh);
+                s += "    const double " + x + " = " + endq + " + dsel(((GP" +
+                     std::to_string(j) + " ^ DP" + is + ") & " + mk + ") == 0u, 0.0, " +
+                     lit(er.c) + ");\n";
             } else {
                 s += "    const double " + x + " = " + endq + " + dsel(" + gq + " == " + di +
                      ", 0.0, " + lit(er.c) + ");\n";
             }
             xs.push_back(x);
         }
+        return xs;
+    };
+    // Software pipelining (o.ahead = D): the relaxation terms of task t over
+    // predecessors placed at least D positions earlier are emitted next to
+    // the dependent per-device chain of task t - D, so the two interleave.
+    // Status codes are still applied in try_place order inside the tail.
+    const int D = std::max(0, o.ahead);
+    std::vector<std::string> early(V);
+    auto head = [&](int i) {
+        const std::string is = std::to_string(i), di = "d" + is;
+        s += "    // " + p.task_ids[p.order[i]] + "\n";
+        // genes were range-checked and clamped when the row was staged
+        s += "    const int " + di + " = " + (greg ? gexpr(i) : "g[" + is + "]") + ";\n";
+        if (greg && !preds[i].empty())
+            s += "    const hs_u32 DP" + is + " = (hs_u32)" + di + " * 0x55555555u;\n";
+        if (l.cls) s += "    int nl" + is + " = 0;\n";
+        // early terms: predecessors placed at or before i - D - 1 (in edge
+        // order; the max over them is exact in any order)
+        std::vector<std::string> xs;
+        for (size_t k = 0; k < preds[i].size(); ++k)
+            if (preds[i][k] <= i - D - 1) {
+                auto t = edge_terms(i, int(k), int(k) + 1);
+                xs.push_back(t[0]);
+            }
+        if (!xs.empty()) early[i] = max_tree(xs, is + "e");
+    };
+    auto tail = [&](int i) {
+        const std::string is = std::to_string(i), di = "d" + is;
+        // try_place order (heuristics.py:92-106): batch size, memory, links,
+        // latency entry; the first failing check decides the status
+        if (!p.all_batch_ok) {
+            std::snprintf(buf, sizeof buf,
+                          "    st = first_status(st, !((0x%llxull >> %s) & 1ull), ST_BATCH);\n",
+                          (unsigned long long)okmask, di.c_str());
+            s += buf;
+        }
+        if (l.mem) {
+            s += "    const hs_u32 M" + is + " = M + " + di + " * " + std::to_string(T * 8) +
+                 ";\n";
+            s += "    const double m" + is + " = ld_shared_f64(M" + is + ");\n";
+            s += "    st = first_status(st, m" + is + " + " + lit(p.extra[i]) + " > CAP[" +
+                 di + "], ST_MEMORY);\n";
+        }
+        std::vector<std::string> xs;
+        for (size_t k = 0; k < preds[i].size(); ++k)
+            if (preds[i][k] > i - D - 1) {
+                auto t = edge_terms(i, int(k), int(k) + 1);
+                xs.push_back(t[0]);
+            }
+        if (!early[i].empty()) xs.push_back(early[i]);
         if (l.cls) s += "    st = first_status(st, nl" + is + ", ST_LINK);\n";
         if (!p.latency_complete) {
             uint64_t miss = 0;
@@ -337,28 +463,11 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 s += buf;
             }
         }
-        // max over predecessors: a balanced tree (no NaN can occur, so max
-        // is associative and the result equals the reference's fold)
         const std::string r = "r" + is;
-        if (xs.empty()) {
+        if (xs.empty())
             s += "    const double " + r + " = 0.0;\n";
-        } else {
-            int lvl = 0;
-            while (xs.size() > 1) {
-                std::vector<std::string> nx;
-                for (size_t k = 0; k + 1 < xs.size(); k += 2) {
-                    const std::string m = "m" + is + "_" + std::to_string(lvl) + "_" +
-                                          std::to_string(k);
-                    s += "    const double " + m + " = " + mx + "(" + xs[k] + ", " +
-                         xs[k + 1] + ");\n";
-                    nx.push_back(m);
-                }
-                if (xs.size() & 1) nx.push_back(xs.back());
-                xs.swap(nx);
-                ++lvl;
-            }
-            s += "    const double " + r + " = " + xs[0] + ";\n";  // max(0.0, x) == x
-        }
+        else
+            s += "    const double " + r + " = " + max_tree(xs, is) + ";\n";  // max(0.0, x) == x
         std::vector<std::string> av, du;
         for (int k = 0; k < K; ++k) {
             av.push_back("a" + std::to_string(k));
@@ -396,6 +505,10 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         if (l.mem)
             s += "    st_shared_f64(M" + is + ", m" + is + " + " + lit(p.extra[i]) + ");\n";
+    };
+    for (int t = 0; t < V + D; ++t) {
+        if (t < V) head(t);
+        if (t - D >= 0) tail(t - D);
     }
     s += "    double ms = 0.0;\n";
     for (int k = 0; k < K; ++k)
@@ -408,10 +521,33 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                   "    st_out = st;\n}\n");
     s += buf;
     (void)checks;
+    // pack16 over the row's 32-bit words (4 genes each) -> GPA[NP]
+    auto pack_words = [&](const std::string &w) {
+        std::string out = "    hs_u32 GPA[" + std::to_string(NP) + "];\n";
+        for (int j = 0; j < NP; ++j) {
+            std::string args;
+            for (int q = 0; q < 4; ++q) {
+                const int k = 4 * j + q;
+                args += (q ? ", " : "") + (k < NW ? w + std::to_string(k) : std::string("0u"));
+            }
+            out += "    GPA[" + std::to_string(j) + "] = pack16(" + args + ");\n";
+        }
+        return out;
+    };
     s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
-         "bool valid, int gene_bad, double &ms, int &st) {\n"
-         "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st);\n  }\n};\n";
+         "bool valid, int gene_bad, double &ms, int &st) {\n";
+    if (greg) {
+        // the staged row was sanitised by eval_tiles: every byte <= K-1
+        s += "    const hs_u32 *GW = reinterpret_cast<const hs_u32 *>(g);\n";
+        for (int k = 0; k < NW; ++k)
+            s += "    const hs_u32 w" + std::to_string(k) + " = GW[" + std::to_string(k) + "];\n";
+        s += pack_words("w");
+        s += "    jit_body<TRACE>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st);\n";
+    } else {
+        s += "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st);\n";
+    }
+    s += "  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
          "  extern __shared__ __align__(16) hs_u8 smem[];\n";
     if (l.dur) s += stage(l.dur_off, "dur", int64_t(V) * K * 8);
@@ -428,6 +564,67 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
                   "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n", T, T);
     s += buf;
+    if (greg) {
+        // Direct-load kernel: no genome tile and no CTA barrier per tile.
+        // Each thread reads its own row from global memory (L1-cached
+        // 32-bit loads: a warp's 32 rows are one contiguous span), clamps
+        // and flags genes >= K, packs them into registers and evaluates;
+        // shared memory holds only the tables and the per-lane state, so
+        // several CTAs share an SM.
+        std::snprintf(buf, sizeof buf,
+                      "extern \"C\" __global__ void __launch_bounds__(%d, %d) "
+                      "hs_jit_direct(const EvalParams a) {\n"
+                      "  extern __shared__ __align__(16) hs_u8 smem[];\n", T, std::max(1, o.ctas));
+        s += buf;
+        if (l.dur) s += stage(l.dur_off, "dur", int64_t(V) * K * 8);
+        if (l.cls) {
+            s += stage(l.ctab_off, "ctab", int64_t(V) * p.n_cls * 8);
+            s += stage(l.bcl_off, "bclass", int64_t(K) * K * 2);
+        }
+        if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
+        s += "  __syncthreads();\n"
+             "  const int li = threadIdx.x;\n"
+             "  double bc = kinf();\n  hs_i64 bi = 0x7fffffffffffffffll;\n"
+             "  const hs_i64 stride = (hs_i64)gridDim.x * blockDim.x;\n";
+        std::snprintf(buf, sizeof buf, "  const hs_u32 kmax = 0x%08xu;\n",
+                      unsigned(K - 1) * 0x01010101u);
+        s += buf;
+        s += "  for (hs_i64 cand = (hs_i64)blockIdx.x * blockDim.x + li; cand < a.n; "
+             "cand += stride) {\n"
+             "    const hs_u32 *rw = reinterpret_cast<const hs_u32 *>(a.genes + cand * a.ld);\n";
+        for (int k = 0; k < NW; ++k)
+            s += "    hs_u32 w" + std::to_string(k) + " = __ldg(rw + " + std::to_string(k) +
+                 ");\n";
+        // the next row of this thread into L2 while this one computes
+        s += "    if (cand + stride < a.n) {\n"
+             "      const hs_u8 *nx = a.genes + (cand + stride) * a.ld;\n";
+        for (int off = 0; off < 4 * NW; off += 128)
+            s += "      asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(nx + " +
+                 std::to_string(off) + "));\n";
+        s += "      asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(nx + " +
+             std::to_string(4 * NW - 1) + "));\n    }\n";
+        s += "    hs_u32 over = 0u;\n";
+        for (int k = 0; k < NW; ++k) {
+            const std::string w = "w" + std::to_string(k);
+            std::string ov = "__vcmpgtu4(" + w + ", kmax)";
+            if (k == NW - 1 && (V & 3)) {
+                char mk[32];
+                std::snprintf(mk, sizeof mk, "0x%xu", (1u << (8 * (V & 3))) - 1u);
+                ov = "(" + ov + " & " + mk + ")";
+            }
+            s += "    over |= " + ov + ";\n    " + w + " = __vminu4(" + w + ", kmax);\n";
+        }
+        s += pack_words("w");
+        s += "    double ms;\n    int st;\n"
+             "    jit_body<false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st);\n"
+             "    if (a.makespan) a.makespan[cand] = ms;\n"
+             "    if (a.status) a.status[cand] = (hs_u8)st;\n"
+             "    const double key = (ms != ms) ? kinf() : ms;\n"
+             "    const hs_i64 gidx = a.index_base + cand;\n"
+             "    if (best_less(key, gidx, bc, bi)) {\n      bc = key;\n      bi = gidx;\n    }\n"
+             "  }\n"
+             "  if (a.best) reduce_best(bc, bi, a.partial, a.ticket, a.best);\n}\n";
+    }
     return next;
 }
 
@@ -514,6 +711,19 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     if (e == cudaSuccess)
         e = cudaKernelSetAttributeForDevice(
             m->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
+    if (e == cudaSuccess && o.genes_reg && p.K <= 4) {
+        m->smem_direct = size_t(m->smem_tile);
+        e = cudaLibraryGetKernel(&m->kern_direct, m->lib, "hs_jit_direct");
+        if (e == cudaSuccess)
+            e = cudaKernelSetAttributeForDevice(m->kern_direct,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(m->smem_direct), device);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &m->blocks_per_sm_direct, (const void *)m->kern_direct, T, m->smem_direct);
+        if (e == cudaSuccess && m->blocks_per_sm_direct < 1)
+            e = cudaErrorInvalidConfiguration;
+    }
     if (e != cudaSuccess) {
         if (m->lib) cudaLibraryUnload(m->lib);
         delete m;
@@ -538,12 +748,18 @@ void jit_free(JitModule *m) {
     delete m;
 }
 
+bool jit_direct_ok(const JitModule &m, const hsk::EvalParams &a) {
+    return m.kern_direct && !a.starts && !a.gen && !a.packed && a.ld % 4 == 0 &&
+           (reinterpret_cast<uintptr_t>(a.genes) & 3) == 0;
+}
+
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid, cudaStream_t stream,
                std::string *err) {
     void *args[] = {(void *)&a};
-    const cudaKernel_t k = a.starts ? m.kern_trace : m.kern;
+    const bool direct = jit_direct_ok(m, a);
+    const cudaKernel_t k = a.starts ? m.kern_trace : direct ? m.kern_direct : m.kern;
     cudaError_t e = cudaLaunchKernel((const void *)k, dim3(grid), dim3(m.T), args,
-                                     m.smem, stream);
+                                     direct ? m.smem_direct : m.smem, stream);
     if (e != cudaSuccess) {
         if (err) *err = std::string("specialised eval launch: ") + cudaGetErrorString(e);
         return HS_ECUDA;

@@ -12,13 +12,18 @@ namespace hs {
 
 // Code-generation choices (HS_JIT_OPTS="regs=20,win=48,avail=reg,dur=sel")
 struct JitOpts {
-    // defaults from the B200 A/B sweep (profiles/README.md, r1c)
+    // defaults from the B200 A/B sweeps (profiles/README.md, r1c and r1g)
     int reg_budget = 64;   // end times kept in registers at once
     int reg_window = 400;  // ... when consumed within this many positions
     bool avail_smem = true;   // per-device available times in shared memory
     bool dur_smem = true;     // latency table in shared memory (else selects)
     bool int_max = false;     // max via int64 compare of bit patterns
+    bool genes_reg = false;   // genes 2 bits each in registers (K <= 4)
+    int near = 8;             // > 0: split residency (registers for consumers
+                              // within `near` positions, long storage beyond)
     int lanes = 256;          // threads (= candidates) per CTA, at most
+    int ahead = 2;            // software pipelining distance (tasks)
+    int ctas = 1;             // CTAs per SM the direct-load kernel is built for
     bool dbuf = true;         // (set by jit_build) double-buffered genome tile
     static JitOpts from_env();
 };
@@ -27,6 +32,9 @@ struct JitModule {
     int device = -1;
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr, kern_trace = nullptr;
+    cudaKernel_t kern_direct = nullptr;  // genes from global into registers
+    size_t smem_direct = 0;
+    int blocks_per_sm_direct = 0;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;
     int64_t smem_tile = 0, smem_tile2 = 0, smem_ends = 0, smem_kstate = 0;
@@ -40,6 +48,8 @@ bool jit_eligible(const Plan &p);
 int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src);
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err);
 void jit_free(JitModule *m);
+// the launch may use the direct-load kernel (explicit u8 genes, 4-aligned)
+bool jit_direct_ok(const JitModule &m, const hsk::EvalParams &a);
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid,
                cudaStream_t stream, std::string *err);
 

@@ -3,7 +3,7 @@
     python tools/quick_perf.py ws200 tf96 ...   (QP_N candidates, QP_JIT=0
     for the ahead-of-time kernel, HS_JIT_OPTS for code-generation options)
 
-Median of 3 blocks of 10 launches over QP_N explicit genomes (default
+Median of QP_BLOCKS (5) blocks of 10 launches over QP_N explicit genomes (default
 2**24, larger than L2), plus one block of on-device generated candidates.
 """
 import json
@@ -38,7 +38,7 @@ for name in sys.argv[1:] or ["ws200"]:
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     blocks = []
-    for _ in range(3):
+    for _ in range(int(os.environ.get("QP_BLOCKS", 5))):
         e0.record()
         for _ in range(10):
             plan.eval(genes, ms, None, best)
@@ -46,6 +46,7 @@ for name in sys.argv[1:] or ["ws200"]:
         torch.cuda.synchronize()
         blocks.append(e0.elapsed_time(e1) / 10 / 1e3)
     dt = statistics.median(blocks)
+    dmin = min(blocks)
     e0.record()
     for _ in range(5):
         plan.eval_gen(N.GEN_RANDOM, 1, 0, n, best=best)
@@ -53,7 +54,7 @@ for name in sys.argv[1:] or ["ws200"]:
     torch.cuda.synchronize()
     dg = e0.elapsed_time(e1) / 5 / 1e3
     print(f"{name} [{tag}]: V={plan.V} explicit {n / dt:.3e} cand/s "
-          f"({dt * 1e3:.2f} ms, blocks {[round(b * 1e3, 2) for b in blocks]})"
+          f"({dt * 1e3:.2f} ms, best {n / dmin:.3e}, blocks {[round(b * 1e3, 2) for b in blocks]})"
           f"  gen {n / dg:.3e} cand/s", flush=True)
     del genes
     torch.cuda.empty_cache()
