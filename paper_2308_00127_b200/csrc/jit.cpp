@@ -117,6 +117,7 @@ JitOpts JitOpts::from_env() {
             if (k == "near") o.near = std::atoi(v.c_str());
             if (k == "ctas") o.ctas = std::max(1, std::atoi(v.c_str()));
             if (k == "ahead") o.ahead = std::atoi(v.c_str());
+            if (k == "fma") o.fma = std::atoi(v.c_str()) != 0;
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -358,6 +359,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         return xs[0];
     };
+    std::vector<double> cconst;  // fma communication constants (HSC[])
     // one relaxation term end(q) + comm(q -> i) per predecessor
     auto edge_terms = [&](int i, int k0, int k1) {
         const std::string is = std::to_string(i), di = "d" + is;
@@ -387,6 +389,17 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             } else if (er.c == 0.0 && !std::signbit(er.c)) {
                 // zero-byte output: end + 0.0 == end for end >= +0
                 s += "    const double " + x + " = " + endq + ";\n";
+            } else if (o.fma && std::isfinite(er.c) && !greg) {
+                // end + (same ? 0 : c) as fma(c, 0.0 or 1.0, end): one FP64
+                // op and one 32-bit select instead of an add and a 64-bit
+                // select; exact: c*1 + end rounds once like end + c, and
+                // c*0 + end == end for finite c and end >= +0
+                // the constant comes from constant memory (an operand of
+                // DFMA, no register moves)
+                s += "    const double " + x + " = __fma_rn(HSC[" +
+                     std::to_string(cconst.size()) + "], dsel(" + gq + " == " + di +
+                     ", 0.0, 1.0), " + endq + ");\n";
+                cconst.push_back(er.c);
             } else if (greg) {
                 // same device <=> the 2-bit fields agree: one LOP3 per edge
                 const int j = q >> 4, sh = 2 * (q & 15);
@@ -534,6 +547,14 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         return out;
     };
+    if (!cconst.empty()) {
+        std::string decl = "__constant__ double HSC[" + std::to_string(cconst.size()) + "] = {";
+        for (size_t k = 0; k < cconst.size(); ++k)
+            decl += (k ? ", " : "") + lit(cconst[k]);
+        decl += "};\n";
+        const size_t at = s.find("template <bool TRACE>");
+        s.insert(at, decl);
+    }
     s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
          "bool valid, int gene_bad, double &ms, int &st) {\n";
