@@ -336,6 +336,28 @@ def main():
         except Exception:
             traffic = None
 
+    # ---- secondary: candidates generated on the device (random_search /
+    # ModuleSolver sweeps): no genome bytes from HBM at all
+    gen_rate = None
+    try:
+        for _ in range(2):
+            plan.eval_gen(N.GEN_RANDOM, 7, 0, n, best=best, stream=stream)
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        reps = max(3, min(args.steps, 10))
+        g0.record(stream)
+        for r in range(reps):
+            plan.eval_gen(N.GEN_RANDOM, 7, r * n, n, best=best, stream=stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gen_rate = {"value": world * n * reps / (g0.elapsed_time(g1) / 1e3),
+                    "unit": UNIT,
+                    "what": "hs_eval_gen: splitmix64 counter-hash genomes "
+                            "generated in shared memory by the evaluating "
+                            "lane (oracle.gen_genes), best only"}
+    except Exception as exc:  # reported, never fatal for the bench
+        gen_rate = {"error": repr(exc)}
+
     # ---- e2e through the C ABI with host buffers (pinned): the genomes go
     # host -> device every step, makespans + best come back every step
     e2e = None
@@ -419,7 +441,8 @@ def main():
                      "kernel_ms": kern_ms,
                      "kernel": "hs_jit_eval" if jit_ms is not None
                      else "hs::eval_kernel"},
-        "cpu_baseline": cpu, "e2e": e2e, "time_to_solution": tts,
+        "cpu_baseline": cpu, "e2e": e2e, "on_device_generation": gen_rate,
+        "time_to_solution": tts,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }

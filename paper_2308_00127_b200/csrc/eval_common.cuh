@@ -359,7 +359,10 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
                 issue_tile(a, tile + gridDim.x, b ? gtile : smem + a.smem_tile2,
                            b ? bar : bar + 1);
         } else {
-            __syncthreads();  // the previous tile's genomes are no longer read
+            // generated rows are written and read by their own lane only:
+            // no CTA barrier, so generation (IMAD pipe) of one warp overlaps
+            // the evaluation (ALU / FP64 / LSU) of the others
+            if (!a.gen) __syncthreads();  // the previous tile is no longer read
             if (a.gen) {
                 if (tid < rows) {
                     hs_u8 *r8 = gtile + (hs_i64)tid * a.ld_s;
@@ -410,7 +413,7 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
                     }
                 }
             }
-            __syncthreads();
+            if (!a.gen) __syncthreads();
         }
         const int li = tid;
         const hs_i64 cand = c0 + li;
