@@ -114,7 +114,31 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
         l = std::min<int64_t>(l, 256);
         return int(l / 32 * 32);
     };
-    const int la = lanes_for(p.lay.eval_bytes), lb = lanes_for(0);
+    int la = lanes_for(p.lay.eval_bytes), lb = lanes_for(0);
+    // Graphs whose live end times leave fewer than kMinLanes lanes per SM
+    // (WS1000: 478 slots = 3.8 KB per candidate, one warp) keep the slots in
+    // global memory instead -- an L2-resident [slot][lane] array per CTA,
+    // coalesced like the shared-memory one -- so several warps share an SM
+    // and hide its latency; shared memory then holds tiles and tables.
+    constexpr int kMinLanes = 128;
+    if (!p.batched && std::max(la, lb) < kMinLanes && slot_bytes > 0) {
+        const int64_t pl = ds->ld_cap + (ds->kt == 0 ? int64_t(16) * p.K : 0);
+        // lanes per CTA bound the scratch footprint (SMs x lanes x slots x
+        // 8 B) that has to stay L2-resident
+        int64_t cap_l = 256;
+        if (const char *v = getenv("HS_GSLOT_LANES")) cap_l = std::max(32, atoi(v));
+        auto lanes_g = [&](int64_t plan_bytes) {
+            int64_t l = (budget - plan_bytes) / pl;
+            l = std::min<int64_t>(l, cap_l);
+            return int(l / 32 * 32);
+        };
+        const int ga = lanes_g(p.lay.eval_bytes), gb = lanes_g(0);
+        if (std::max(ga, gb) > std::max(la, lb)) {
+            ds->ends_global = true;
+            la = ga;
+            lb = gb;
+        }
+    }
     // plan tables in shared memory unless that costs more than one warp
     ds->plan_smem = la >= 32 && la >= lb - 32;
     ds->T = ds->plan_smem ? la : lb;
@@ -123,7 +147,7 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
         ds->smem_tile = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0);
         ds->smem_ends = ds->smem_tile +
                         ((int64_t(ds->T) * ds->ld_cap + 15) & ~int64_t(15));
-        ds->smem_kstate = ds->smem_ends + slot_bytes * ds->T;
+        ds->smem_kstate = ds->smem_ends + (ds->ends_global ? 0 : slot_bytes * ds->T);
         ds->smem = ds->smem_kstate +
                    (ds->kt == 0 ? int64_t(2) * p.K * ds->T * 8 : 0);
         int blocks = 0;
@@ -154,6 +178,17 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
         delete ds;
         if (err) *err = std::string("plan upload: ") + cudaGetErrorString(e);
         return HS_ECUDA;
+    }
+    if (ds->ends_global) {
+        // the per-launch slot scratch (tens of MB) comes from the device's
+        // default stream-ordered pool: keep freed blocks in the pool instead
+        // of unmapping them at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
     }
     if ((int)p.devs.size() <= dev) p.devs.resize(dev + 1, nullptr);
     p.devs[dev] = ds;
@@ -278,6 +313,13 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     }
     a.smem_ends = jm ? jm->smem_ends : ds->smem_ends;
     a.smem_kstate = jm ? jm->smem_kstate : ds->smem_kstate;
+    Scratch ends_g;
+    ends_g.s = stream;
+    if ((jm ? jm->ends_global : ds->ends_global) && n > 0) {
+        a.ends_g_cta = int64_t(jm ? jm->slots : p.live_slots) * lanes;
+        CK(cudaMallocAsync(&ends_g.ptr, size_t(grid) * size_t(a.ends_g_cta) * 8, stream));
+        a.ends_g = static_cast<double *>(ends_g.ptr);
+    }
     if (jm) {
         a.slots = jm->slots;
         rc = hs::jit_launch(*jm, a, grid, stream, &err);

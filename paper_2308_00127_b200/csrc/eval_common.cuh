@@ -96,6 +96,11 @@ struct EvalParams {
     hs_i64 smem_tile;   // byte offsets in shared memory: genome tile,
     hs_i64 smem_ends;   // [slot][lane] end times,
     hs_i64 smem_kstate; // [2K][lane] device state (generic K)
+    // global-memory tier of the end-time slots (graphs whose live end times
+    // do not fit shared memory): CTA b owns ends_g[b * ends_g_cta ...],
+    // laid out [slot][lane] like the shared-memory slots (coalesced)
+    double *ends_g;
+    hs_i64 ends_g_cta;
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)

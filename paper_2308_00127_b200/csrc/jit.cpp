@@ -118,6 +118,7 @@ JitOpts JitOpts::from_env() {
             if (k == "ctas") o.ctas = std::max(1, std::atoi(v.c_str()));
             if (k == "ahead") o.ahead = std::atoi(v.c_str());
             if (k == "fma") o.fma = std::atoi(v.c_str()) != 0;
+            if (k == "glanes") o.gslot_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -129,7 +130,7 @@ static int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 // Straight-line code grows with V + E and ptxas time super-linearly
 // (minutes at V ~ 1000), so very large graphs stay on the AOT kernel.
-constexpr int kJitMaxV = 512, kJitMaxE = 2048, kJitMaxK = 64;
+constexpr int kJitMaxV = 1100, kJitMaxE = 2600, kJitMaxK = 64;
 
 bool jit_eligible(const Plan &p) {
     return !p.batched && p.K <= kJitMaxK && !p.nan_possible && p.V > 0 &&
@@ -149,6 +150,7 @@ struct JitLayout {
 JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap,
                      bool dbuf = true) {
     JitLayout l;
+    if (o.gslots) slots = 0;  // end-time slots in global memory
     l.dbuf = dbuf;
     l.dur = o.dur_smem || p.K > 4;
     l.avail = o.avail_smem || p.K > 4;
@@ -179,6 +181,7 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
 int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap,
                        bool dbuf) {
     const bool avail = o.avail_smem || p.K > 4;
+    if (o.gslots) slots = 0;
     return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
 }
 
@@ -296,9 +299,14 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
          std::string(greg ? "const hs_u32 *GPA" : "const hs_u8 *g") +
          ", int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
-         "double &ms_out, int &st_out) {\n";
-    s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
-         ") + li;\n    (void)E;\n";
+         "double &ms_out, int &st_out, double *EG) {\n";
+    // end-time slots [slot][lane]: shared memory, or this CTA's region of
+    // the global-memory tier (graphs whose live end times exceed it)
+    if (o.gslots)
+        s += "    double *E = EG + li;\n    (void)E;\n";
+    else
+        s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
+             ") + li;\n    (void)E;\n";
     if (l.dur)
         s += "    const double *DUR = reinterpret_cast<const double *>(smem + " +
              std::to_string(l.dur_off) + ");\n";
@@ -555,7 +563,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         const size_t at = s.find("template <bool TRACE>");
         s.insert(at, decl);
     }
-    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts;\n"
+    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
          "bool valid, int gene_bad, double &ms, int &st) {\n";
     if (greg) {
@@ -564,9 +572,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int k = 0; k < NW; ++k)
             s += "    const hs_u32 w" + std::to_string(k) + " = GW[" + std::to_string(k) + "];\n";
         s += pack_words("w");
-        s += "    jit_body<TRACE>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st);\n";
+        s += "    jit_body<TRACE>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
     } else {
-        s += "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st);\n";
+        s += "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
     }
     s += "  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
@@ -578,6 +586,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     }
     if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
     s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
+         "  body.eg = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
          "  eval_tiles(a, smem, body);\n}\n";
     std::snprintf(buf, sizeof buf,
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
@@ -604,6 +613,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
         s += "  __syncthreads();\n"
+             "  double *EGC = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
              "  const int li = threadIdx.x;\n"
              "  double bc = kinf();\n  hs_i64 bi = 0x7fffffffffffffffll;\n"
              "  const hs_i64 stride = (hs_i64)gridDim.x * blockDim.x;\n";
@@ -637,7 +647,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         s += pack_words("w");
         s += "    double ms;\n    int st;\n"
-             "    jit_body<false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st);\n"
+             "    jit_body<false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC);\n"
              "    if (a.makespan) a.makespan[cand] = ms;\n"
              "    if (a.status) a.status[cand] = (hs_u8)st;\n"
              "    const double key = (ms != ms) ? kinf() : ms;\n"
@@ -673,14 +683,31 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
                                      o.lanes) / 32 * 32);
     };
     // double-buffer the genome tile only when it costs no lanes
-    const bool dbuf = lanes_for(true) >= lanes_for(false);
+    bool dbuf = lanes_for(true) >= lanes_for(false);
     int T = lanes_for(dbuf);
+    JitOpts oe = o;
+    // too few lanes with the end times in shared memory: move them to the
+    // global-memory tier ([slot][lane] per CTA, L2-resident; `gslot_lanes`
+    // bounds the footprint SMs x lanes x slots x 8 B)
+    if (T < 128 && slots > 0) {
+        JitOpts og = o;
+        og.gslots = true;
+        auto lanes_g = [&](bool db) {
+            return int(std::min<int64_t>(budget / per_lane_bytes(p, og, slots, ld_cap, db),
+                                         std::min(o.lanes, o.gslot_lanes)) / 32 * 32);
+        };
+        const bool dg = lanes_g(true) >= lanes_g(false);
+        if (lanes_g(dg) > T) {
+            oe.gslots = true;
+            dbuf = dg;
+            T = lanes_g(dg);
+        }
+    }
     if (T < 32) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
     }
     std::string src;
-    JitOpts oe = o;
     oe.dbuf = dbuf;
     jit_emit(p, T, oe, &src);
     const char *hdr_src[] = {kEvalCommonSrc};
@@ -713,9 +740,10 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->T = m->lanes = T;
     m->slots = slots;
     m->ld_cap = ld_cap;
-    m->opts = o;
+    m->opts = oe;
+    m->ends_global = oe.gslots;
     {
-        const JitLayout l = jit_layout(p, o, T, slots, ld_cap, dbuf);
+        const JitLayout l = jit_layout(p, oe, T, slots, ld_cap, dbuf);
         m->smem_tile = l.tile;
         m->smem_tile2 = l.tile2;
         m->smem_ends = l.ends;

@@ -26,6 +26,8 @@ struct JitOpts {
     bool fma = false;         // communication term as one fma (exact)
     int ctas = 1;             // CTAs per SM the direct-load kernel is built for
     bool dbuf = true;         // (set by jit_build) double-buffered genome tile
+    bool gslots = false;      // (set by jit_build) end-time slots in global memory
+    int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
     static JitOpts from_env();
 };
 
@@ -35,6 +37,7 @@ struct JitModule {
     cudaKernel_t kern = nullptr, kern_trace = nullptr;
     cudaKernel_t kern_direct = nullptr;  // genes from global into registers
     size_t smem_direct = 0;
+    bool ends_global = false;  // end-time slots in global memory
     int blocks_per_sm_direct = 0;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;

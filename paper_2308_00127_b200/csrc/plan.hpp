@@ -99,6 +99,7 @@ struct DevState {
     size_t smem = 0;          // dynamic shared memory per CTA
     int64_t smem_tile = 0, smem_ends = 0, smem_kstate = 0;
     int kt = 0;               // K template (2,3,4) or 0 = generic K
+    bool ends_global = false; // end-time slots in global memory (L2 tier)
 };
 
 // Batched-variant options: allowed sub-batch sizes (null = L/4, L/2, 3L/4,

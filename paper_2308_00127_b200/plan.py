@@ -160,13 +160,15 @@ class Plan:
 
     def maybe_specialize(self, n: int) -> bool:
         """Specialise when a batch is large enough to amortise the compile
-        (HS_JIT_MIN candidates, default 2**20); False if out of scope."""
+        (HS_JIT_MIN candidates, default 2**20; 2**27 above 512 tasks, where
+        NVRTC takes tens of seconds); False if out of scope."""
         import os
         if self.specialized_ms is not None:
             return True
         if os.environ.get("HS_JIT", "1") == "0":
             return False
-        if n < int(os.environ.get("HS_JIT_MIN", 1 << 20)):
+        floor = 1 << (20 if self.V <= 512 else 27)
+        if n < int(os.environ.get("HS_JIT_MIN", floor)):
             return False
         if not self.jit_eligible():
             return False

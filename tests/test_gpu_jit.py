@@ -152,3 +152,33 @@ def test_specialised_large_vs_c_oracle(name, oracle_lib):
     gg = O.gen_genes(5, 77, 4096, plan.V, plan.K)
     assert np.array_equal(out.cpu().numpy(), gg)
     assert np.array_equal(gms.cpu().numpy(), O.fitness_np(tb, gg)[0])
+
+
+@pytest.mark.parametrize("name", ["ws1000", "ws_stack_10x100"])
+def test_specialised_large_graphs(name, oracle_lib):
+    """~1000-task graphs: WS1000 keeps its 478 live end times in the
+    global-memory slot tier, the 10x100 stack in shared memory."""
+    doc = instance_doc(name)
+    g, hw, t = hs.load_instance(doc)
+    plan = get_plan(g, hw, t, 1)
+    assert plan.jit_eligible()
+    plan.specialize()
+    for case in doc["cases"]:
+        if case["L"] != 1 or case.get("order"):
+            continue
+        genes = case_genes(case)
+        ms, st = hs.fitness_batch(torch.from_numpy(genes).cuda(), g, hw, t, 1,
+                                  return_status=True)
+        assert _hexes(ms.cpu().numpy(), st.cpu().numpy()) == case["expected"]
+    tb = O.build_tables(O.Instance.from_doc(doc), 1)
+    n = 40_000
+    genes = np.random.default_rng(8).integers(plan.K, size=(n, plan.V),
+                                              dtype=np.uint8)
+    want, wst = CTables(tb).fitness(oracle_lib, genes, threads=8)
+    ms, st = hs.fitness_batch(torch.from_numpy(genes).cuda(), g, hw, t, 1,
+                              return_status=True)
+    assert np.array_equal(st.cpu().numpy(), wst)
+    assert np.array_equal(ms.cpu().numpy().view(np.uint64),
+                          want.view(np.uint64))
+    cost, idx = hs.argmin_batch(torch.from_numpy(genes).cuda(), g, hw, t, 1)
+    assert (cost, idx) == O.argmin_first(want)
