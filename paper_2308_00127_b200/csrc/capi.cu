@@ -400,9 +400,9 @@ int hs_plan_specialize(const hs_plan *plan, double *compile_ms) {
     }
     if (!hs::jit_eligible(p))
         return set_err(HS_EINVAL, "plan not eligible for the specialised "
-                                  "evaluator (needs K <= 4, one bandwidth over "
-                                  "a full mesh, no capacity / batch-size / "
-                                  "missing-entry / NaN cases)");
+                                  "evaluator (needs a non-batched plan with "
+                                  "K <= 64, V <= 1100, E <= 2600 and no NaN "
+                                  "in the cost model)");
     hs::JitModule *m = nullptr;
     std::string err;
     int rc = hs::jit_build(p, dev, &m, &err);

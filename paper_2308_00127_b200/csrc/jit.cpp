@@ -11,9 +11,11 @@
 // (heuristics.py:43-148); results are checked bit-for-bit against the
 // golden fixtures by the same GPU tests as the AOT kernel.
 //
-// Scope (everything else uses the AOT kernel): K <= 4 devices, one
-// bandwidth over a full mesh, and no capacity / batch-size / missing-entry /
-// NaN cases (plan flags clear) -- the benchmark graphs of the paper.
+// Scope (everything else uses the AOT kernel): non-batched plans with
+// K <= 64 devices, V <= 1100 tasks, E <= 2600 edges and no NaN anywhere in
+// the cost model (max is then associative, so predecessor maxima may be
+// reordered). Capacity, batch-size, missing-entry and missing-link checks
+// are emitted only when the plan needs them.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
