@@ -121,6 +121,7 @@ JitOpts JitOpts::from_env() {
             if (k == "ahead") o.ahead = std::atoi(v.c_str());
             if (k == "fma") o.fma = std::atoi(v.c_str()) != 0;
             if (k == "glanes") o.gslot_lanes = std::max(32, std::atoi(v.c_str()));
+            if (k == "sync") o.sync = std::atoi(v.c_str());
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -298,7 +299,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
     const bool greg = o.genes_reg && K <= 4;
     const int NP = (V + 15) / 16, NW = (V + 3) / 4;
-    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
+    s += "template <bool TRACE, bool SYNC>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
          std::string(greg ? "const hs_u32 *GPA" : "const hs_u8 *g") +
          ", int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
          "double &ms_out, int &st_out, double *EG) {\n";
@@ -529,9 +530,17 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         if (l.mem)
             s += "    st_shared_f64(M" + is + ", m" + is + " + " + lit(p.extra[i]) + ");\n";
     };
+    // Optional CTA barrier every `sync` tasks (tile driver only, where every
+    // thread of the CTA runs the body) to keep the warps of a CTA within one
+    // window of the straight-line code. Measured (profiles r1h): no gain on
+    // WS1000, whose fetch stalls come from the code streaming through the
+    // instruction caches once per tile, and a loss on WS200 -- off by default.
+    const int sync_every = std::max(0, o.sync);
     for (int t = 0; t < V + D; ++t) {
         if (t < V) head(t);
         if (t - D >= 0) tail(t - D);
+        if (sync_every && t % sync_every == sync_every - 1 && t + 1 < V + D)
+            s += "    if (SYNC) __syncthreads();\n";
     }
     s += "    double ms = 0.0;\n";
     for (int k = 0; k < K; ++k)
@@ -574,9 +583,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int k = 0; k < NW; ++k)
             s += "    const hs_u32 w" + std::to_string(k) + " = GW[" + std::to_string(k) + "];\n";
         s += pack_words("w");
-        s += "    jit_body<TRACE>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
+        s += "    jit_body<TRACE, true>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
     } else {
-        s += "    jit_body<TRACE>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
+        s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
     }
     s += "  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
@@ -649,7 +658,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         s += pack_words("w");
         s += "    double ms;\n    int st;\n"
-             "    jit_body<false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC);\n"
+             "    jit_body<false, false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC);\n"
              "    if (a.makespan) a.makespan[cand] = ms;\n"
              "    if (a.status) a.status[cand] = (hs_u8)st;\n"
              "    const double key = (ms != ms) ? kinf() : ms;\n"

@@ -27,6 +27,7 @@ struct JitOpts {
     int ctas = 1;             // CTAs per SM the direct-load kernel is built for
     bool dbuf = true;         // (set by jit_build) double-buffered genome tile
     bool gslots = false;      // (set by jit_build) end-time slots in global memory
+    int sync = 0;             // CTA barrier every `sync` tasks (0: none)
     int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
     static JitOpts from_env();
 };
