@@ -325,6 +325,7 @@ def main():
     alg_bytes = n * (V + 8)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
+    sm_util = None
     prof = os.path.join(ROOT, "profiles", "eval_kernel_traffic.json")
     if os.path.exists(prof):
         try:
@@ -333,6 +334,7 @@ def main():
             traffic = tp.get("dram_bytes_per_candidate")
             if traffic is not None:
                 traffic = traffic * n
+            sm_util = tp.get("sm_utilisation")
         except Exception:
             traffic = None
 
@@ -440,7 +442,10 @@ def main():
                      "algorithmic_bytes_per_candidate": V + 8,
                      "kernel_ms": kern_ms,
                      "kernel": "hs_jit_eval" if jit_ms is not None
-                     else "hs::eval_kernel"},
+                     else "hs::eval_kernel",
+                     # the pipes that actually bound the kernel (ncu, one
+                     # launch of the same kernel)
+                     "sm_utilisation": sm_util},
         "cpu_baseline": cpu, "e2e": e2e, "on_device_generation": gen_rate,
         "time_to_solution": tts,
         "gpu_launches": args.steps,
