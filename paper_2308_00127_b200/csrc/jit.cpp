@@ -571,7 +571,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (size_t k = 0; k < cconst.size(); ++k)
             decl += (k ? ", " : "") + lit(cconst[k]);
         decl += "};\n";
-        const size_t at = s.find("template <bool TRACE>");
+        const size_t at = s.find("template <bool TRACE");
         s.insert(at, decl);
     }
     s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg;\n"

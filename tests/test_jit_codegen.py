@@ -63,3 +63,18 @@ def test_scope():
     assert Plan(*hs.load_instance(instance_doc("ws1000")), 1).jit_eligible()
     assert all(Plan(*hs.load_instance(d), d["L"]).jit_eligible()
                for d in random_docs()[:50] if d["graph"]["tasks"])
+
+
+@pytest.mark.parametrize("opts", ["fma=1", "genes=reg", "near=0,ahead=0",
+                                  "sync=16", "avail=reg,dur=sel",
+                                  "max=int,ahead=4"])
+def test_emit_options_compile(opts, monkeypatch):
+    """Every code-generation option of the specialiser (HS_JIT_OPTS) emits
+    CUDA that NVRTC accepts for sm_100a."""
+    if not os.path.exists("/usr/local/cuda/lib64/libnvrtc.so.12"):
+        pytest.skip("NVRTC not available")
+    monkeypatch.setenv("HS_JIT_OPTS", opts)
+    p = Plan(*hs.load_instance(instance_doc("ws30")), 1)
+    src = p.specialized_source(64)
+    rc, log = _nvrtc_compile(src)
+    assert rc == 0, (opts, log[-2000:])
