@@ -122,6 +122,7 @@ JitOpts JitOpts::from_env() {
             if (k == "fma") o.fma = std::atoi(v.c_str()) != 0;
             if (k == "glanes") o.gslot_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "sync") o.sync = std::atoi(v.c_str());
+            if (k == "gword") o.gword = std::atoi(v.c_str()) != 0;
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -437,7 +438,17 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         const std::string is = std::to_string(i), di = "d" + is;
         s += "    // " + p.task_ids[p.order[i]] + "\n";
         // genes were range-checked and clamped when the row was staged
-        s += "    const int " + di + " = " + (greg ? gexpr(i) : "g[" + is + "]") + ";\n";
+        if (!greg && o.gword) {
+            // one 32-bit shared-memory load per four genes (1 wavefront
+            // instead of 4), bytes extracted in registers
+            if ((i & 3) == 0)
+                s += "    const hs_u32 GWD" + std::to_string(i >> 2) +
+                     " = reinterpret_cast<const hs_u32 *>(g)[" + std::to_string(i >> 2) + "];\n";
+            s += "    const int " + di + " = (int)((GWD" + std::to_string(i >> 2) + " >> " +
+                 std::to_string(8 * (i & 3)) + ") & 0xFFu);\n";
+        } else {
+            s += "    const int " + di + " = " + (greg ? gexpr(i) : "g[" + is + "]") + ";\n";
+        }
         if (greg && !preds[i].empty())
             s += "    const hs_u32 DP" + is + " = (hs_u32)" + di + " * 0x55555555u;\n";
         if (l.cls) s += "    int nl" + is + " = 0;\n";
