@@ -121,7 +121,7 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
     // coalesced like the shared-memory one -- so several warps share an SM
     // and hide its latency; shared memory then holds tiles and tables.
     constexpr int kMinLanes = 128;
-    if (!p.batched && std::max(la, lb) < kMinLanes && slot_bytes > 0) {
+    if (std::max(la, lb) < kMinLanes && slot_bytes > 0) {
         const int64_t pl = ds->ld_cap + (ds->kt == 0 ? int64_t(16) * p.K : 0);
         // lanes per CTA bound the scratch footprint (SMs x lanes x slots x
         // 8 B) that has to stay L2-resident
@@ -316,7 +316,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     Scratch ends_g;
     ends_g.s = stream;
     if ((jm ? jm->ends_global : ds->ends_global) && n > 0) {
-        a.ends_g_cta = int64_t(jm ? jm->slots : p.live_slots) * lanes;
+        a.ends_g_cta = int64_t(jm ? jm->slots : p.live_slots) * (p.batched ? p.P : 1) * lanes;
         CK(cudaMallocAsync(&ends_g.ptr, size_t(grid) * size_t(a.ends_g_cta) * 8, stream));
         a.ends_g = static_cast<double *>(ends_g.ptr);
     }

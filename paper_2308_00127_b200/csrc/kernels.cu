@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(512) beval_kernel(const EvalParams a) {
     body.bdur_ok = plan + a.lay.bdur_ok;
     body.ctab = reinterpret_cast<const double *>(plan + a.lay.ctab);
     body.bclass = reinterpret_cast<const hs_u16 *>(plan + a.lay.bclass);
-    body.ends = reinterpret_cast<double *>(smem + a.smem_ends);
+    body.ends = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta
+                         : reinterpret_cast<double *>(smem + a.smem_ends);
     body.kstate = reinterpret_cast<double *>(smem + a.smem_kstate);
     body.starts = a.starts;
     body.lanes = a.lanes;

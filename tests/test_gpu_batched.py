@@ -91,3 +91,32 @@ def test_generated_extended_genomes():
     allw = np.array([B.eval_one(inst, 4, opts, r)[0] for r in allg])
     assert (cost, idx) == O.argmin_first(allw)
     assert best == [int(x) for x in allg[idx]]
+
+
+def test_global_slot_tier_ws200():
+    """WS200 at L=4 (3 parts per task): the per-part end times overflow
+    shared memory and live in the global-memory slot tier."""
+    from conftest import instance_doc
+    doc = instance_doc("ws200")
+    g, hw, t = hs.load_instance(doc)
+    inst = O.Instance.from_doc(doc)
+    opts = B.options(inst, 4)
+    rng = np.random.default_rng(4)
+    genes = rng.integers(len(opts), size=(300, len(g.tasks)), dtype=np.uint8)
+    genes[1, 5] = len(opts)  # out of range -> GraphError status
+    want = [B.eval_one(inst, 4, opts, row) for row in genes]
+    ms, st = hs.fitness_batched(torch.from_numpy(genes).cuda(), g, hw, t, 4,
+                                return_status=True)
+    ms, st = ms.cpu().numpy(), st.cpu().numpy()
+    for r, (wm, ws) in enumerate(want):
+        assert st[r] == ws, r
+        if ws == 0:
+            assert fhex(ms[r]) == fhex(wm), r
+    # generated extended genomes through the same tier
+    plan = get_plan(g, hw, t, 4, None, ())
+    n = 500
+    gm = torch.empty(n, dtype=torch.float64, device="cuda")
+    plan.eval_gen(N.GEN_RANDOM, 9, 0, n, makespan=gm)
+    gg = O.gen_genes(9, 0, n, plan.V, len(opts))
+    assert [fhex(x) for x in gm.cpu().numpy()] == \
+        [fhex(B.eval_one(inst, 4, opts, r)[0]) for r in gg]
