@@ -112,6 +112,12 @@ __device__ __forceinline__ double pymax(double a, double b) {
     return b > a ? b : a;  // Python max(a, b): a unless b > a
 }
 
+// (p && v > r) ? v : r -- one compare with a predicate input and a 64-bit
+// select (the specialised kernel's dominance-pruned relaxation term)
+__device__ __forceinline__ double maxsel(double r, bool p, double v) {
+    return (p & (v > r)) ? v : r;
+}
+
 // Python max(a, b) for a, b >= +0.0 and not NaN: the binary64 bit patterns
 // of non-negative doubles order like the values (ALU compare, not FP64)
 __device__ __forceinline__ double pymax_nn(double a, double b) {

@@ -123,6 +123,7 @@ JitOpts JitOpts::from_env() {
             if (k == "glanes") o.gslot_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "sync") o.sync = std::atoi(v.c_str());
             if (k == "gword") o.gword = std::atoi(v.c_str()) != 0;
+            if (k == "dom") o.dom = std::atoi(v.c_str()) != 0;
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -372,6 +373,19 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         return xs[0];
     };
     std::vector<double> cconst;  // fma communication constants (HSC[])
+    // Dominance pruning (uniform bandwidth, o.dom): a predecessor on the
+    // consumer's device contributes end + 0.0, which never exceeds the
+    // device's available time (per-device ends never decrease without NaN,
+    // and every time is >= +0.0), so max(ready, avail) is unchanged when it
+    // is dropped. Each producer then carries one value f = end + om/beta
+    // (one add per producer instead of per edge) and each edge is one
+    // predicated compare-and-select: acc = (d_q != d_i && f > acc) ? f : acc.
+    const bool dom = o.dom && !l.cls && !greg;
+    std::vector<double> prod_c(V, 0.0);
+    for (int i = 0; i < V; ++i)
+        for (int e = p.nodes[i].e_begin; e < p.nodes[i].e_end; ++e)
+            prod_c[p.edges[e].gpos] = p.edges[e].c;
+    auto zero_c = [&](int q) { return prod_c[q] == 0.0 && !std::signbit(prod_c[q]); };
     // one relaxation term end(q) + comm(q -> i) per predecessor
     auto edge_terms = [&](int i, int k0, int k1) {
         const std::string is = std::to_string(i), di = "d" + is;
@@ -387,6 +401,12 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 : in_reg ? "d" + std::to_string(q)
                 : "(int)g[" + std::to_string(q) + "]";
             const std::string x = "x" + is + "_" + std::to_string(k);
+            if (dom) {
+                // the producer's f (register name f<q>, or its slot)
+                const std::string fq = in_reg ? "f" + std::to_string(q) : endq;
+                xs.push_back((zero_c(q) ? std::string() : gq + " != " + di) + "|" + fq);
+                continue;
+            }
             if (l.cls) {
                 // comm class of (producer device, consumer device); 0xFFFF =
                 // missing link (core.py:153-154), class 0 = same device
@@ -428,6 +448,31 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         return xs;
     };
+    // dom: fold "cond|value" terms into a running maximum named `acc`
+    auto fold = [&](const std::vector<std::string> &terms, const std::string &acc,
+                    const std::string &init) {
+        size_t k0 = 0;
+        if (init == "0.0" && !terms.empty()) {
+            // first term against the 0.0 start: a plain select (v >= +0.0)
+            const size_t bar = terms[0].find('|');
+            const std::string cond = terms[0].substr(0, bar), v = terms[0].substr(bar + 1);
+            s += "    double " + acc + " = " +
+                 (cond.empty() ? v : "dsel(" + cond + ", " + v + ", 0.0)") + ";\n";
+            k0 = 1;
+        } else {
+            s += "    double " + acc + " = " + init + ";\n";
+        }
+        for (size_t k = k0; k < terms.size(); ++k) {
+            const std::string &t = terms[k];
+            const size_t bar = t.find('|');
+            const std::string cond = t.substr(0, bar), v = t.substr(bar + 1);
+            if (cond.empty())
+                s += "    " + acc + " = " + mx + "(" + acc + ", " + v + ");\n";
+            else
+                s += "    " + acc + " = maxsel(" + acc + ", " + cond + ", " + v + ");\n";
+        }
+        return acc;
+    };
     // Software pipelining (o.ahead = D): the relaxation terms of task t over
     // predecessors placed at least D positions earlier are emitted next to
     // the dependent per-device chain of task t - D, so the two interleave.
@@ -460,7 +505,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 auto t = edge_terms(i, int(k), int(k) + 1);
                 xs.push_back(t[0]);
             }
-        if (!xs.empty()) early[i] = max_tree(xs, is + "e");
+        if (!xs.empty())
+            early[i] = dom ? fold(xs, "re" + is, "0.0") : max_tree(xs, is + "e");
     };
     auto tail = [&](int i) {
         const std::string is = std::to_string(i), di = "d" + is;
@@ -485,7 +531,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
                 auto t = edge_terms(i, int(k), int(k) + 1);
                 xs.push_back(t[0]);
             }
-        if (!early[i].empty()) xs.push_back(early[i]);
+        if (!early[i].empty() && !dom) xs.push_back(early[i]);
         if (l.cls) s += "    st = first_status(st, nl" + is + ", ST_LINK);\n";
         if (!p.latency_complete) {
             uint64_t miss = 0;
@@ -499,7 +545,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             }
         }
         const std::string r = "r" + is;
-        if (xs.empty())
+        if (dom)
+            fold(xs, r, early[i].empty() ? "0.0" : early[i]);
+        else if (xs.empty())
             s += "    const double " + r + " = 0.0;\n";
         else
             s += "    const double " + r + " = " + max_tree(xs, is) + ";\n";  // max(0.0, x) == x
@@ -527,8 +575,14 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         std::snprintf(buf, sizeof buf,
                       "    if (TRACE && valid) starts[cand * %d + %d] = %s;\n", V, i, si.c_str());
         s += buf;
+        std::string stored = ei;
+        if (dom && last[i] >= 0) {
+            stored = "f" + is;
+            s += "    const double " + stored + " = " +
+                 (zero_c(i) ? ei : ei + " + " + lit(prod_c[i])) + ";\n";
+        }
         if (where[i] >= 0)
-            s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + ei + ";\n";
+            s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + stored + ";\n";
         if (l.avail) {
             s += "    st_shared_f64(" + Ai + ", " + ei + ");\n";
         } else {

@@ -23,6 +23,7 @@ struct JitOpts {
                               // within `near` positions, long storage beyond)
     int lanes = 256;          // threads (= candidates) per CTA, at most
     int ahead = 2;            // software pipelining distance (tasks)
+    bool dom = true;          // drop same-device predecessor terms (dominated)
     bool gword = false;       // genes read four per 32-bit shared-memory load
     bool fma = false;         // communication term as one fma (exact)
     int ctas = 1;             // CTAs per SM the direct-load kernel is built for
