@@ -112,6 +112,26 @@ __device__ __forceinline__ double pymax(double a, double b) {
     return b > a ? b : a;  // Python max(a, b): a unless b > a
 }
 
+// Tensor-memory tier of the specialised kernel's end-time slots: each
+// thread owns one TMEM lane (its warp's lane quadrant) and a band of
+// columns; a double is two 32-bit columns. tcgen05.ld/st are asynchronous:
+// loads are waited before use (tm_wait_ld, registers tied to the wait),
+// stores are waited before any later load of the same columns (tm_wait_st).
+__device__ __forceinline__ void tm_st2(hs_u32 addr, double v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};"
+                 ::"r"(addr), "r"(__double2loint(v)), "r"(__double2hiint(v)) : "memory");
+}
+__device__ __forceinline__ void tm_ld2(hs_u32 addr, hs_u32 &lo, hs_u32 &hi) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                 : "=r"(lo), "=r"(hi) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double tm_val(hs_u32 lo, hs_u32 hi) {
+    return __hiloint2double((int)hi, (int)lo);
+}
+
 // (p && v > r) ? v : r -- one compare with a predicate input and a 64-bit
 // select (the specialised kernel's dominance-pruned relaxation term)
 __device__ __forceinline__ double maxsel(double r, bool p, double v) {

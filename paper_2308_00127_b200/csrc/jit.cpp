@@ -124,6 +124,9 @@ JitOpts JitOpts::from_env() {
             if (k == "sync") o.sync = std::atoi(v.c_str());
             if (k == "gword") o.gword = std::atoi(v.c_str()) != 0;
             if (k == "dom") o.dom = std::atoi(v.c_str()) != 0;
+            if (k == "tmem") o.tmem = std::atoi(v.c_str()) != 0;
+            if (k == "tlanes") o.tm_lanes = std::max(32, std::atoi(v.c_str()));
+            if (k == "tregs") o.tm_regs = std::max(0, std::atoi(v.c_str()));
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -155,7 +158,7 @@ struct JitLayout {
 JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_cap,
                      bool dbuf = true) {
     JitLayout l;
-    if (o.gslots) slots = 0;  // end-time slots in global memory
+    if (o.gslots || o.tmem) slots = 0;  // end-time slots in global / tensor memory
     l.dbuf = dbuf;
     l.dur = o.dur_smem || p.K > 4;
     l.avail = o.avail_smem || p.K > 4;
@@ -186,7 +189,7 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
 int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap,
                        bool dbuf) {
     const bool avail = o.avail_smem || p.K > 4;
-    if (o.gslots) slots = 0;
+    if (o.gslots || o.tmem) slots = 0;
     return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
 }
 
@@ -207,7 +210,9 @@ std::string stage(int64_t dst, const char *section, int64_t bytes) {
 }  // namespace
 
 // Emits the kernel for T lanes; returns the number of shared-memory slots.
-int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
+int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
+    JitOpts o = o_in;
+    if (o.tm_cols <= 0) o.tmem = false;  // TMEM columns are chosen by jit_build
     const int V = p.V, K = p.K;
     const int reg_budget = o.reg_budget, reg_window = o.reg_window;
     std::vector<int> last(V, -1);
@@ -304,7 +309,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     s += "template <bool TRACE, bool SYNC>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
          std::string(greg ? "const hs_u32 *GPA" : "const hs_u8 *g") +
          ", int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
-         "double &ms_out, int &st_out, double *EG) {\n";
+         "double &ms_out, int &st_out, double *EG, hs_u32 TB) {\n";
     // end-time slots [slot][lane]: shared memory, or this CTA's region of
     // the global-memory tier (graphs whose live end times exceed it)
     if (o.gslots)
@@ -396,6 +401,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             const bool in_reg = where[q] == -1 || (near > 0 && i - q <= near);
             const std::string endq = in_reg
                 ? "e" + std::to_string(q)
+                : o.tmem ? "TV" + is + "_" + std::to_string(q)  // loaded by tm_loads()
                 : "E[" + std::to_string((long long)where[q] * T) + "]";
             const std::string gq = greg ? gexpr(q)
                 : in_reg ? "d" + std::to_string(q)
@@ -479,6 +485,35 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     // Status codes are still applied in try_place order inside the tail.
     const int D = std::max(0, o.ahead);
     std::vector<std::string> early(V);
+    // TMEM tier: load every slot-resident predecessor value of task i that
+    // is read by the early terms, then one wait with the registers tied to it
+    auto tm_loads = [&](int i) {
+        std::vector<int> qs;
+        for (size_t k = 0; k < preds[i].size(); ++k) {
+            const int q = preds[i][k];
+            if (q > i - D - 1) continue;  // late term: a register value
+            const bool in_reg = where[q] == -1 || (near > 0 && i - q <= near);
+            if (!in_reg) qs.push_back(q);
+        }
+        const std::string is = std::to_string(i);
+        for (size_t c = 0; c < qs.size(); c += 8) {
+            std::string outs;
+            for (size_t k = c; k < std::min(qs.size(), c + 8); ++k) {
+                const std::string v = "TV" + is + "_" + std::to_string(qs[k]);
+                s += "    hs_u32 " + v + "l, " + v + "h;\n";
+                s += "    tm_ld2(TB + " + std::to_string(2 * where[qs[k]]) + ", " + v + "l, " + v +
+                     "h);\n";
+                outs += std::string(outs.empty() ? "" : ", ") + "\"+r\"(" + v + "l), \"+r\"(" + v +
+                        "h)";
+            }
+            s += "    asm volatile(\"tcgen05.wait::ld.sync.aligned;\" : " + outs +
+                 " :: \"memory\");\n";
+            for (size_t k = c; k < std::min(qs.size(), c + 8); ++k) {
+                const std::string v = "TV" + is + "_" + std::to_string(qs[k]);
+                s += "    const double " + v + " = tm_val(" + v + "l, " + v + "h);\n";
+            }
+        }
+    };
     auto head = [&](int i) {
         const std::string is = std::to_string(i), di = "d" + is;
         s += "    // " + p.task_ids[p.order[i]] + "\n";
@@ -497,6 +532,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         if (greg && !preds[i].empty())
             s += "    const hs_u32 DP" + is + " = (hs_u32)" + di + " * 0x55555555u;\n";
         if (l.cls) s += "    int nl" + is + " = 0;\n";
+        if (o.tmem) tm_loads(i);
         // early terms: predecessors placed at or before i - D - 1 (in edge
         // order; the max over them is exact in any order)
         std::vector<std::string> xs;
@@ -581,8 +617,12 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
             s += "    const double " + stored + " = " +
                  (zero_c(i) ? ei : ei + " + " + lit(prod_c[i])) + ";\n";
         }
-        if (where[i] >= 0)
-            s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + stored + ";\n";
+        if (where[i] >= 0) {
+            if (o.tmem)
+                s += "    tm_st2(TB + " + std::to_string(2 * where[i]) + ", " + stored + ");\n";
+            else
+                s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + stored + ";\n";
+        }
         if (l.avail) {
             s += "    st_shared_f64(" + Ai + ", " + ei + ");\n";
         } else {
@@ -602,6 +642,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     // instruction caches once per tile, and a loss on WS200 -- off by default.
     const int sync_every = std::max(0, o.sync);
     for (int t = 0; t < V + D; ++t) {
+        // a slot written at step q + D is read at step >= q + near + 1:
+        // waiting for the stores every 4 steps orders them when near >= D + 4
+        if (o.tmem && t % 4 == 0 && t > 0) s += "    tm_wait_st();\n";
         if (t < V) head(t);
         if (t - D >= 0) tail(t - D);
         if (sync_every && t % sync_every == sync_every - 1 && t + 1 < V + D)
@@ -639,7 +682,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         const size_t at = s.find("template <bool TRACE");
         s.insert(at, decl);
     }
-    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg;\n"
+    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg; hs_u32 tb;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
          "bool valid, int gene_bad, double &ms, int &st) {\n";
     if (greg) {
@@ -648,9 +691,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         for (int k = 0; k < NW; ++k)
             s += "    const hs_u32 w" + std::to_string(k) + " = GW[" + std::to_string(k) + "];\n";
         s += pack_words("w");
-        s += "    jit_body<TRACE, true>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
+        s += "    jit_body<TRACE, true>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg, tb);\n";
     } else {
-        s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg);\n";
+        s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg, tb);\n";
     }
     s += "  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
@@ -663,7 +706,32 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
     if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
     s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
          "  body.eg = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
-         "  eval_tiles(a, smem, body);\n}\n";
+         "  body.tb = 0u;\n";
+    if (o.tmem) {
+        // the whole TMEM of the SM (one CTA per SM): warp 0 allocates 512
+        // columns; each warp uses its lane quadrant and a column band
+        s += "  __shared__ hs_u32 tm_base_s;\n"
+             "  if (threadIdx.x < 32) {\n"
+             "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" "
+             ":: \"r\"(smem_addr(&tm_base_s)) : \"memory\");\n"
+             "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\" ::: \"memory\");\n"
+             "  }\n"
+             "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
+             "  __syncthreads();\n"
+             "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n";
+        s += "  body.tb = tm_base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16) + (threadIdx.x >> 7) * " +
+             std::to_string(o.tm_cols) + "u;\n";
+    }
+    s += "  eval_tiles(a, smem, body);\n";
+    if (o.tmem)
+        s += "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
+             "  __syncthreads();\n"
+             "  if (threadIdx.x < 32) {\n"
+             "    asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+             "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" "
+             ":: \"r\"(tm_base_s) : \"memory\");\n"
+             "  }\n";
+    s += "}\n";
     std::snprintf(buf, sizeof buf,
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
                   "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
@@ -723,7 +791,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src) {
         }
         s += pack_words("w");
         s += "    double ms;\n    int st;\n"
-             "    jit_body<false, false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC);\n"
+             "    jit_body<false, false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC, 0u);\n"
              "    if (a.makespan) a.makespan[cand] = ms;\n"
              "    if (a.status) a.status[cand] = (hs_u8)st;\n"
              "    const double key = (ms != ms) ? kinf() : ms;\n"
@@ -754,19 +822,21 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     const int ld_cap = p.pref_ld() + 16;
     const int64_t head = head_bytes(p, o);
     const int64_t budget = int64_t(optin) - head - 1024;
+    JitOpts ob = o;  // slots in shared memory
+    ob.tmem = false;
     auto lanes_for = [&](bool db) {
-        return int(std::min<int64_t>(budget / per_lane_bytes(p, o, slots, ld_cap, db),
+        return int(std::min<int64_t>(budget / per_lane_bytes(p, ob, slots, ld_cap, db),
                                      o.lanes) / 32 * 32);
     };
     // double-buffer the genome tile only when it costs no lanes
     bool dbuf = lanes_for(true) >= lanes_for(false);
     int T = lanes_for(dbuf);
-    JitOpts oe = o;
+    JitOpts oe = ob;
     // too few lanes with the end times in shared memory: move them to the
     // global-memory tier ([slot][lane] per CTA, L2-resident; `gslot_lanes`
     // bounds the footprint SMs x lanes x slots x 8 B)
     if (T < 128 && slots > 0) {
-        JitOpts og = o;
+        JitOpts og = ob;
         og.gslots = true;
         auto lanes_g = [&](bool db) {
             return int(std::min<int64_t>(budget / per_lane_bytes(p, og, slots, ld_cap, db),
@@ -779,6 +849,41 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
             T = lanes_g(dg);
         }
     }
+    // tensor-memory tier (o.tmem): the end-time slots move to TMEM (512
+    // columns x 128 lanes per SM), shared memory keeps tiles and tables
+    // with its own lane count and long-lived register budget (more warps,
+    // fewer registers each); otherwise the shared-memory sizing above stands
+    int n_slots = slots;
+    if (o.tmem && !oe.gslots && slots > 0) {
+        JitOpts ot = o;
+        ot.lanes = o.tm_lanes;
+        ot.reg_budget = o.tm_regs;
+        const int slots_t = jit_emit(p, 32, ot, nullptr);
+        auto lanes_t = [&](bool db) {
+            return int(std::min<int64_t>(budget / per_lane_bytes(p, ot, slots_t, ld_cap, db),
+                                         ot.lanes) / 32 * 32);
+        };
+        const bool dt = lanes_t(true) >= lanes_t(false);
+        const int Tt = std::min(lanes_t(dt), 512);
+        const int groups = (Tt / 32 + 3) / 4;
+        const int cols = groups > 0 ? (512 / groups) & ~1 : 0;
+        if (Tt >= 32 && slots_t > 0 && 2 * slots_t <= cols) {
+            oe = ot;
+            oe.tm_cols = cols;
+            dbuf = dt;
+            T = Tt;
+            n_slots = slots_t;
+        } else if (Tt >= 32 && slots_t == 0) {
+            // every end time fits the smaller register budget: the same
+            // 12-warp configuration without any slot tier
+            oe = ot;
+            oe.tmem = false;
+            dbuf = dt;
+            T = Tt;
+            n_slots = 0;
+        }
+    }
+    oe.tmem = oe.tmem && oe.tm_cols > 0;
     if (T < 32) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
@@ -814,12 +919,13 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     JitModule *m = new JitModule();
     m->device = device;
     m->T = m->lanes = T;
-    m->slots = slots;
+    m->slots = n_slots;
     m->ld_cap = ld_cap;
     m->opts = oe;
     m->ends_global = oe.gslots;
+    m->tmem = oe.tmem;
     {
-        const JitLayout l = jit_layout(p, oe, T, slots, ld_cap, dbuf);
+        const JitLayout l = jit_layout(p, oe, T, n_slots, ld_cap, dbuf);
         m->smem_tile = l.tile;
         m->smem_tile2 = l.tile2;
         m->smem_ends = l.ends;
@@ -859,6 +965,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     m->blocks_per_sm = std::max(1, std::min(2048 / T, int(smem_sm / (m->smem + 1024))));
+    if (m->tmem) m->blocks_per_sm = 1;  // each CTA allocates all 512 TMEM columns
     m->sms = sms;
     m->src_bytes = src.size();
     m->compile_ms = std::chrono::duration<double, std::milli>(

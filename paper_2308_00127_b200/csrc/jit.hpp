@@ -30,6 +30,10 @@ struct JitOpts {
     bool dbuf = true;         // (set by jit_build) double-buffered genome tile
     bool gslots = false;      // (set by jit_build) end-time slots in global memory
     int sync = 0;             // CTA barrier every `sync` tasks (0: none)
+    bool tmem = true;         // end-time slots in tensor memory (TMEM) when they fit
+    int tm_lanes = 384;       // lanes per CTA with TMEM slots (12 warps)
+    int tm_regs = 32;         // long-lived end times in registers with TMEM slots
+    int tm_cols = 0;          // (set by jit_build) TMEM columns per warp group
     int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
     static JitOpts from_env();
 };
@@ -41,6 +45,7 @@ struct JitModule {
     cudaKernel_t kern_direct = nullptr;  // genes from global into registers
     size_t smem_direct = 0;
     bool ends_global = false;  // end-time slots in global memory
+    bool tmem = false;         // end-time slots in tensor memory
     int blocks_per_sm_direct = 0;
     int T = 0, lanes = 0, slots = 0, ld_cap = 0, blocks_per_sm = 1, sms = 0;
     size_t smem = 0;
