@@ -127,6 +127,9 @@ JitOpts JitOpts::from_env() {
             if (k == "tmem") o.tmem = std::atoi(v.c_str()) != 0;
             if (k == "tlanes") o.tm_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "tregs") o.tm_regs = std::max(0, std::atoi(v.c_str()));
+            // emission-only (hs_plan_emit_specialized): TMEM columns per warp
+            // group, normally chosen by jit_build
+            if (k == "tcols") o.tm_cols = std::max(0, std::atoi(v.c_str()));
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;

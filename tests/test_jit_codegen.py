@@ -67,7 +67,8 @@ def test_scope():
 
 @pytest.mark.parametrize("opts", ["fma=1", "genes=reg", "near=0,ahead=0",
                                   "sync=16", "avail=reg,dur=sel",
-                                  "max=int,ahead=4"])
+                                  "max=int,ahead=4", "dom=0",
+                                  "tmem=1,tcols=170,regs=8"])
 def test_emit_options_compile(opts, monkeypatch):
     """Every code-generation option of the specialiser (HS_JIT_OPTS) emits
     CUDA that NVRTC accepts for sm_100a."""
