@@ -32,7 +32,7 @@ struct JitOpts {
     int sync = 0;             // CTA barrier every `sync` tasks (0: none)
     bool tmem = true;         // end-time slots in tensor memory (TMEM) when they fit
     int tm_lanes = 384;       // lanes per CTA with TMEM slots (12 warps)
-    int tm_regs = 32;         // long-lived end times in registers with TMEM slots
+    int tm_regs = 40;         // long-lived end times in registers with TMEM slots
     int tm_cols = 0;          // (set by jit_build) TMEM columns per warp group
     int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
     static JitOpts from_env();
