@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--e2e-n", type=int, default=1 << 23)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
+    ap.add_argument("--no-others", action="store_true",
+                    help="skip the other graph families' throughputs")
     ap.add_argument("--no-jit", action="store_true",
                     help="time the ahead-of-time kernel instead of the "
                          "graph-specialised one")
@@ -360,6 +362,44 @@ def main():
     except Exception as exc:  # reported, never fatal for the bench
         gen_rate = {"error": repr(exc)}
 
+    # ---- the paper's other graph families (device-resident explicit
+    # genomes, same kernel family; reported beside the headline workload)
+    others = {}
+    if not args.no_others:
+        for name in ("ws30", "rn50f", "iv3f", "tf96", "ws_stack_10x20"):
+            try:
+                with open(os.path.join(ROOT, "tests", "golden", "instances",
+                                       name + ".json")) as f:
+                    od = json.load(f)
+                og, ohw, ot = hs.load_instance(od)
+                op = get_plan(og, ohw, ot, 1)
+                if op.jit_eligible():
+                    op.specialize()
+                on = 1 << 22
+                ogen = torch.randint(0, op.K, (on, op.pref_ld),
+                                     dtype=torch.uint8, device="cuda",
+                                     generator=gen)
+                ob = torch.empty(2, dtype=torch.int64, device="cuda")
+                om = torch.empty(on, dtype=torch.float64, device="cuda")
+                for _ in range(2):
+                    op.eval(ogen, om, None, ob, stream=stream)
+                o0 = torch.cuda.Event(enable_timing=True)
+                o1 = torch.cuda.Event(enable_timing=True)
+                o0.record(stream)
+                for _ in range(5):
+                    op.eval(ogen, om, None, ob, stream=stream)
+                o1.record(stream)
+                torch.cuda.synchronize()
+                others[name] = {"value": world * on * 5 /
+                                (o0.elapsed_time(o1) / 1e3), "unit": UNIT,
+                                "V": op.V, "K": op.K,
+                                "kernel": "hs_jit_eval" if op.jit_eligible()
+                                else "hs::eval_kernel"}
+                del ogen, om
+            except Exception as exc:  # reported, never fatal for the bench
+                others[name] = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+
     # ---- e2e through the C ABI with host buffers (pinned): the genomes go
     # host -> device every step, makespans + best come back every step
     e2e = None
@@ -447,6 +487,7 @@ def main():
                      # launch of the same kernel)
                      "sm_utilisation": sm_util},
         "cpu_baseline": cpu, "e2e": e2e, "on_device_generation": gen_rate,
+        "other_graphs": others,
         "time_to_solution": tts,
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
