@@ -16,7 +16,7 @@ if [ "${BENCH:-1}" = "1" ]; then
 fi
 if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
-     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --n 4194304 --no-cpu --no-tts --e2e-n 1048576 > /dev/null 2>&1; echo "ncu list rc=$?"
+     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --n 4194304 --no-cpu --no-tts --no-others --e2e-n 1048576 > /dev/null 2>&1; echo "ncu list rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-eval} -s 3 -c 1 \
      -o gpurun_out/${TAG}_eval python tools/quick_perf.py ${NCU_WL:-ws200} > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu full rc=$?"
   tail -3 gpurun_out/${TAG}_ncu.log
