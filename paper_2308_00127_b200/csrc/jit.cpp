@@ -130,6 +130,7 @@ JitOpts JitOpts::from_env() {
             // emission-only (hs_plan_emit_specialized): TMEM columns per warp
             // group, normally chosen by jit_build
             if (k == "tcols") o.tm_cols = std::max(0, std::atoi(v.c_str()));
+            if (k == "dsmem") o.dur_smem_max = std::atoi(v.c_str());
             if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
         }
         at = end + 1;
@@ -153,7 +154,7 @@ namespace {
 // Shared-memory layout of the specialised kernel (byte offsets); every
 // table is staged from the plan blob once per CTA.
 struct JitLayout {
-    bool dur = false, cls = false, mem = false, avail = false, dbuf = true;
+    bool dur = false, durg = false, cls = false, mem = false, avail = false, dbuf = true;
     int64_t dur_off = 0, ctab_off = 0, bcl_off = 0, cap_off = 0, head = 16;
     int64_t tile = 0, tile2 = 0, ends = 0, avail_off = 0, mem_off = 0, total = 0;
 };
@@ -164,6 +165,13 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
     if (o.gslots || o.tmem) slots = 0;  // end-time slots in global / tensor memory
     l.dbuf = dbuf;
     l.dur = o.dur_smem || p.K > 4;
+    // a large latency table (many devices: the transformer case study has
+    // 288 x 30 entries = 69 KB) is read through L1 from the plan blob
+    // instead of occupying shared memory that would otherwise hold lanes
+    if (l.dur && int64_t(p.V) * p.K * 8 > o.dur_smem_max) {
+        l.dur = false;
+        l.durg = true;
+    }
     l.avail = o.avail_smem || p.K > 4;
     l.cls = !p.uniform_comm;
     l.mem = p.mem_check;
@@ -312,7 +320,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
     s += "template <bool TRACE, bool SYNC>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, " +
          std::string(greg ? "const hs_u32 *GPA" : "const hs_u8 *g") +
          ", int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
-         "double &ms_out, int &st_out, double *EG, hs_u32 TB) {\n";
+         "double &ms_out, int &st_out, double *EG, hs_u32 TB, const double *DG) {\n";
     // end-time slots [slot][lane]: shared memory, or this CTA's region of
     // the global-memory tier (graphs whose live end times exceed it)
     if (o.gslots)
@@ -604,8 +612,10 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         } else {
             s += "    const double " + si + " = " + mx + "(" + r + ", " + sel(di, av) + ");\n";
         }
-        std::string dsrc = l.dur ? "DUR[" + std::to_string(i * K) + " + " + di + "]" : sel(di, du);
-        if (l.dur) {
+        std::string dsrc = l.dur    ? "DUR[" + std::to_string(i * K) + " + " + di + "]"
+                           : l.durg ? "__ldg(DG + " + std::to_string(i * K) + " + " + di + ")"
+                                    : sel(di, du);
+        if (l.dur || l.durg) {
             bool same = true;
             for (auto &v : du) same = same && v == du[0];
             if (same) dsrc = du[0];
@@ -685,7 +695,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         const size_t at = s.find("template <bool TRACE");
         s.insert(at, decl);
     }
-    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg; hs_u32 tb;\n"
+    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg; hs_u32 tb;\n  const double *dg;\n"
          "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
          "bool valid, int gene_bad, double &ms, int &st) {\n";
     if (greg) {
@@ -694,9 +704,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         for (int k = 0; k < NW; ++k)
             s += "    const hs_u32 w" + std::to_string(k) + " = GW[" + std::to_string(k) + "];\n";
         s += pack_words("w");
-        s += "    jit_body<TRACE, true>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg, tb);\n";
+        s += "    jit_body<TRACE, true>(smem, GPA, li, cand, valid, gene_bad, starts, ms, st, eg, tb, dg);\n";
     } else {
-        s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg, tb);\n";
+        s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg, tb, dg);\n";
     }
     s += "  }\n};\n";
     s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
@@ -709,7 +719,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
     if (l.mem) s += stage(l.cap_off, "cap", int64_t(K) * 8);
     s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
          "  body.eg = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
-         "  body.tb = 0u;\n";
+         "  body.tb = 0u;\n"
+         "  body.dg = reinterpret_cast<const double *>(a.blob + a.lay.dur);\n";
     if (o.tmem) {
         // the whole TMEM of the SM (one CTA per SM): warp 0 allocates 512
         // columns; each warp uses its lane quadrant and a column band
@@ -794,7 +805,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         }
         s += pack_words("w");
         s += "    double ms;\n    int st;\n"
-             "    jit_body<false, false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC, 0u);\n"
+             "    jit_body<false, false>(smem, GPA, li, cand, true, over != 0u, nullptr, ms, st, EGC, 0u, "
+             "reinterpret_cast<const double *>(a.blob + a.lay.dur));\n"
              "    if (a.makespan) a.makespan[cand] = ms;\n"
              "    if (a.status) a.status[cand] = (hs_u8)st;\n"
              "    const double key = (ms != ms) ? kinf() : ms;\n"

@@ -17,6 +17,8 @@ struct JitOpts {
     int reg_window = 400;  // ... when consumed within this many positions
     bool avail_smem = true;   // per-device available times in shared memory
     bool dur_smem = true;     // latency table in shared memory (else selects)
+    int dur_smem_max = 1 << 30;  // ... up to this many bytes, else read through L1
+                              // (measured slower on tf96: 8.3e8 vs 1.16e9)
     bool int_max = false;     // max via int64 compare of bit patterns
     bool genes_reg = false;   // genes 2 bits each in registers (K <= 4)
     int near = 8;             // > 0: split residency (registers for consumers
