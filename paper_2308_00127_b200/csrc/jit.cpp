@@ -5,11 +5,21 @@
 // the same tile loop as the ahead-of-time kernel (eval_common.cuh).
 //
 // Compared with walking node/edge records, this removes every plan load and
-// address computation from the inner loop, keeps short-lived end times in
-// registers, and lets ptxas schedule the loads of later placements early.
-// The arithmetic is the same binary64 sequence as the reference decoder
-// (heuristics.py:43-148); results are checked bit-for-bit against the
-// golden fixtures by the same GPU tests as the AOT kernel.
+// address computation from the inner loop. On top of that (defaults from
+// the B200 sweeps in profiles/README.md):
+//  * software pipelining: relaxation terms of task t are emitted beside the
+//    dependent per-device chain of task t - ahead;
+//  * split residency: every end time is a register value for consumers
+//    within `near` positions; values read farther away get long storage --
+//    registers (greedy interval selection), then end-time slots in tensor
+//    memory (tcgen05.ld/st, 12 warps/SM), shared memory, or a global-memory
+//    tier for graphs whose live end times exceed the SM;
+//  * dominance pruning: same-device predecessor terms never exceed the
+//    device's available time and are dropped.
+// The arithmetic is the reference decoder's binary64 sequence
+// (heuristics.py:43-148) up to reorderings that are exact without NaN
+// (max is associative); results are checked bit-for-bit against the golden
+// fixtures by the same GPU tests as the AOT kernel.
 //
 // Scope (everything else uses the AOT kernel): non-batched plans with
 // K <= 64 devices, V <= 1100 tasks, E <= 2600 edges and no NaN anywhere in
@@ -140,7 +150,8 @@ JitOpts JitOpts::from_env() {
 
 static int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
-// Straight-line code grows with V + E and ptxas time super-linearly
+// Straight-line code grows with V + E and NVRTC time super-linearly (about
+// 20 s at V ~ 1000 on the GPU box's host)
 // (minutes at V ~ 1000), so very large graphs stay on the AOT kernel.
 constexpr int kJitMaxV = 1100, kJitMaxE = 2600, kJitMaxK = 64;
 
