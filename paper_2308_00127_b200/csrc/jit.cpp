@@ -151,8 +151,8 @@ JitOpts JitOpts::from_env() {
 static int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 // Straight-line code grows with V + E and NVRTC time super-linearly (about
-// 20 s at V ~ 1000 on the GPU box's host)
-// (minutes at V ~ 1000), so very large graphs stay on the AOT kernel.
+// 20 s at V ~ 1000 on the GPU box's host), so larger graphs stay on the AOT
+// kernel.
 constexpr int kJitMaxV = 1100, kJitMaxE = 2600, kJitMaxK = 64;
 
 bool jit_eligible(const Plan &p) {
