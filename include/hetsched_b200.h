@@ -130,7 +130,7 @@ int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
  * latency constants baked in) and compiled by NVRTC for sm_100a (one-time
  * cost, reported in *compile_ms); later hs_eval* calls on this device use
  * it. HS_EINVAL when the plan is outside the specialised scope (batched
- * plans, K > 64, V > 512, E > 2048, or a NaN in the cost model); the
+ * plans, K > 64, V > 1100, E > 2600, or a NaN in the cost model); the
  * ahead-of-time kernel then keeps serving the plan. */
 int hs_plan_specialize(const hs_plan *plan, double *compile_ms);
 /* The CUDA source the specialiser would compile for `lanes` lanes. */
