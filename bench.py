@@ -409,8 +409,11 @@ def main():
     hm = torch.empty(ne, dtype=torch.float64, pin_memory=True)
     hmn = hm.numpy()
     variants = {}
-    for kind in ("packed2", "u8"):
-        if kind == "packed2":
+    for kind in ("packed3", "packed2", "u8"):
+        if kind == "packed3":
+            src = hs.pack_genes3(host_rows)
+            call = plan.eval_host_packed3
+        elif kind == "packed2":
             src = hs.pack_genes(host_rows)
             call = plan.eval_host_packed
         else:
@@ -438,10 +441,11 @@ def main():
                           "h2d_bytes_per_step": int(src.nbytes),
                           "d2h_bytes_per_step": ne * 8 + 16,
                           "candidates_per_step": ne}
-    e2e = dict(variants["packed2"])
-    e2e["api"] = ("hs_eval_host_packed (C ABI): pinned host genomes packed "
-                  "2 bits/gene in, every makespan + best out, chunked "
-                  "H2D/kernel/D2H on 2 streams; wall clock per call")
+    e2e = dict(variants["packed3"])
+    e2e["api"] = ("hs_eval_host_packed3 (C ABI): pinned host genomes packed "
+                  "base-3, 5 genes/byte in, every makespan + best out, "
+                  "chunked H2D/kernel/D2H on 2 streams; wall clock per call")
+    e2e["packed2_genomes"] = variants["packed2"]
     e2e["u8_genomes"] = variants["u8"]
 
     if rank != 0:

@@ -165,6 +165,19 @@ int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
                         int64_t ld, double *h_makespan, uint8_t *h_status,
                         hs_best *h_best, int64_t index_base, void *stream);
 
+/* Base-3 packed genomes (K <= 3, or <= 3 batched options): gene i of a row
+ * is base-3 digit i%5 (least significant first) of byte i/5, i.e. byte j =
+ * sum_d gene[5j+d] * 3^d; rows of `ld` bytes with ceil(V/5) <= ld <=
+ * pref_ld. 1.6 bits per gene (WS200: 41 B per candidate instead of 52 B
+ * 2-bit or 204 B u8) for the PCIe-bound host path; expanded in shared
+ * memory. A byte >= 243 decodes to an out-of-range gene (status 4). */
+int hs_eval_packed3(const hs_plan *plan, const uint8_t *d_packed, int64_t n,
+                    int64_t ld, double *d_makespan, uint8_t *d_status,
+                    hs_best *d_best, int64_t index_base, void *stream);
+int hs_eval_host_packed3(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
+                         int64_t ld, double *h_makespan, uint8_t *h_status,
+                         hs_best *h_best, int64_t index_base, void *stream);
+
 /* On-device candidates: candidate c in [first, first+n) has genes
  * oracle/hs_oracle.py::gen_genes(seed, c). Optional d_genes_out [n x V]. */
 int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,

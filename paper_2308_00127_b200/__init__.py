@@ -16,7 +16,7 @@ from .core import (Device, DnnGraph, GraphError, HardwareSystem,
                    transitive_closure)
 from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
                          fitness, fitness_batch, fitness_batch_packed,
-                         genome_from_map, greedy, met, pack_genes,
+                         genome_from_map, greedy, met, pack_genes, pack_genes3,
                          one_plus_one_ea, random_search, simulated_annealing,
                          specialize, throughput)
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,

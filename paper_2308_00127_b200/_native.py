@@ -94,6 +94,10 @@ def load() -> C.CDLL:
                                          vp]),
             "hs_eval_host_packed": (C.c_int, [vp, vp, i64, i64, vp, vp, vp,
                                               i64, vp]),
+            "hs_eval_packed3": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64,
+                                          vp]),
+            "hs_eval_host_packed3": (C.c_int, [vp, vp, i64, i64, vp, vp, vp,
+                                               i64, vp]),
             "hs_eval_gen": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp,
                                       vp, vp]),
             "hs_eval_gen_ex": (C.c_int, [vp, C.c_int, C.c_uint64, i64, i64,
@@ -122,7 +126,7 @@ def exported_symbols() -> list[str]:
             "hs_plan_batched_options", "hs_plan_get_info", "hs_plan_order",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_packed", "hs_eval_host_packed",
-            "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
+            "hs_eval_packed3", "hs_eval_host_packed3", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
             "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge"]
 
 

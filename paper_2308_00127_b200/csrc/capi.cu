@@ -217,7 +217,16 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     if (!plan) return set_err(HS_EINVAL, "null plan");
     const hs::Plan &p = plan->p;
     if (n < 0) return set_err(HS_EINVAL, "n < 0");
-    if (packed) {
+    if (packed == 2) {
+        // base-3 genes, 5 per byte: rows of ld bytes, 5*ld >= V, at most
+        // the staged tile row (expanded in place)
+        if (p.batched ? p.n_opt > 3 : p.K > 3)
+            return set_err(HS_EINVAL, "base-3 packed genomes need at most 3 gene values");
+        if (n > 0 && p.V > 0 &&
+            (!genes || ld * 5 < p.V || ld > p.pref_ld() || ld > 256))
+            return set_err(HS_EINVAL, "base-3 packed genes must be [n x ld], "
+                                      "5*ld >= V, ld <= preferred stride");
+    } else if (packed) {
         // 2-bit genes: rows of ld bytes, ld a multiple of 4, >= ceil(V/4),
         // at most the staged tile row (expanded in place)
         if (p.batched ? p.n_opt > 4 : p.K > 4)
@@ -681,6 +690,21 @@ int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
                         hs_best *h_best, int64_t index_base, void *stream) {
     return eval_host_impl(plan, h_packed, n, ld, h_makespan, h_status, h_best,
                           index_base, stream, 1);
+}
+
+int hs_eval_packed3(const hs_plan *plan, const uint8_t *d_packed, int64_t n,
+                    int64_t ld, double *d_makespan, uint8_t *d_status,
+                    hs_best *d_best, int64_t index_base, void *stream) {
+    return run_eval(plan, d_packed, n, ld, 0, 0, 0, nullptr, nullptr, 0, d_makespan,
+                    d_status, nullptr, nullptr, d_best, index_base,
+                    static_cast<cudaStream_t>(stream), 2);
+}
+
+int hs_eval_host_packed3(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
+                         int64_t ld, double *h_makespan, uint8_t *h_status,
+                         hs_best *h_best, int64_t index_base, void *stream) {
+    return eval_host_impl(plan, h_packed, n, ld, h_makespan, h_status, h_best,
+                          index_base, stream, 2);
 }
 
 int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,

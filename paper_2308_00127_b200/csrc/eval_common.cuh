@@ -74,7 +74,8 @@ struct EvalParams {
     int plan_smem;
     int lanes, ld_s, slots;
     int bulk;           // genome tiles may use cp.async.bulk
-    int packed;         // genes arrive 2 bits each (K <= 4), `ld` bytes/row
+    int packed;         // 1: genes arrive 2 bits each (K <= 4); 2: base-3,
+                        // 5 per byte (K <= 3); `ld` bytes/row
     const hs_u8 *genes;
     hs_i64 n, ld;
     int gen;            // 1 hash-random, 2 enumerate (K6); 0 staged genes
@@ -417,7 +418,49 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
                 } else {
                     for (hs_i64 b = tid; b < bytes; b += T) dst[b] = src[b];
                 }
-                if (a.packed) {
+                if (a.packed == 2) {
+                    __syncthreads();
+                    // base-3 genes, 5 per byte (least significant digit
+                    // first): 4 row bytes -> 20 genes -> five 4-gene words
+                    hs_u32 pk[64];
+                    const int nb = (int)a.ld;
+                    const int nw = (nb + 3) >> 2;
+                    const hs_u8 *prow = dst + (hs_i64)tid * a.ld;
+#pragma unroll 4
+                    for (int w = 0; w < nw && w < 64; ++w) {
+                        hs_u32 x = 0u;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (tid < rows && 4 * w + j < nb)
+                                x |= (hs_u32)prow[4 * w + j] << (8 * j);
+                        pk[w] = x;
+                    }
+                    __syncthreads();
+                    hs_u32 *orow = reinterpret_cast<hs_u32 *>(gtile + (hs_i64)tid * a.ld_s);
+                    const int nout = a.ld_s >> 2;
+#pragma unroll 2
+                    for (int w = 0; w < nw && w < 64; ++w) {
+                        const hs_u32 x = pk[w];
+                        hs_u32 o[5] = {0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            hs_u32 b = (x >> (8 * j)) & 0xFFu;
+#pragma unroll
+                            for (int d = 0; d < 5; ++d) {
+                                // b / 3 for b < 256; the last digit keeps the
+                                // quotient whole, so a byte >= 243 yields a
+                                // gene >= 3 (flagged out of range)
+                                const hs_u32 q = (b * 171u) >> 9;
+                                const int gi = 5 * j + d;
+                                o[gi >> 2] |= (d < 4 ? b - 3u * q : b) << (8 * (gi & 3));
+                                b = q;
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < 5; ++k)
+                            if (5 * w + k < nout) orow[5 * w + k] = o[k];
+                    }
+                } else if (a.packed) {
                     __syncthreads();
                     // 2-bit genes, 16 per word: word w -> four 4-gene words
                     hs_u32 pk[64];

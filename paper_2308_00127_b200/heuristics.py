@@ -234,10 +234,28 @@ def pack_genes(genes: np.ndarray) -> np.ndarray:
             | (g[:, :, 3] << 6)).astype(np.uint8)
 
 
+def pack_genes3(genes: np.ndarray) -> np.ndarray:
+    """Base-3 packing of uint8 genes < 3 [n, V] -> [n, ceil(V/5)]: byte j =
+    sum_d gene[5j+d] * 3**d (hs_eval_packed3's layout, 1.6 bits per gene)."""
+    genes = np.asarray(genes, np.uint8)
+    n, V = genes.shape
+    if genes.size and genes.max() > 2:
+        raise GraphError("base-3 packing needs genes < 3")
+    pld = (V + 4) // 5
+    g = np.zeros((n, pld * 5), np.uint8)
+    g[:, :V] = genes
+    g = g.reshape(n, pld, 5)
+    return (g[:, :, 0] + 3 * g[:, :, 1] + 9 * g[:, :, 2] + 27 * g[:, :, 3]
+            + 81 * g[:, :, 4]).astype(np.uint8)
+
+
 def fitness_batch_packed(packed, g, hw, table, L: int, *,
-                         return_status: bool = False):
-    """fitness_batch for 2-bit packed genomes (pack_genes): numpy -> host
-    path (a quarter of the PCIe bytes), CUDA tensor -> device path."""
+                         return_status: bool = False, radix: int = 4):
+    """fitness_batch for packed genomes: `radix` 4 = 2-bit (pack_genes),
+    3 = base-3 (pack_genes3). numpy -> host path (a quarter / a fifth of
+    the PCIe bytes), CUDA tensor -> device path."""
+    if radix not in (3, 4):
+        raise ValueError("radix must be 3 or 4")
     plan = get_plan(g, hw, table, L)
     n = int(packed.shape[0])
     plan.maybe_specialize(n)
@@ -245,7 +263,7 @@ def fitness_batch_packed(packed, g, hw, table, L: int, *,
         import torch
         ms = torch.empty(n, dtype=torch.float64, device=packed.device)
         st = torch.empty(n, dtype=torch.uint8, device=packed.device)
-        plan.eval_packed(packed, ms, st)
+        (plan.eval_packed if radix == 4 else plan.eval_packed3)(packed, ms, st)
         if return_status:
             return ms, st
         if n and int(st.max().item()) >= N.ST_MISSING:
@@ -255,7 +273,8 @@ def fitness_batch_packed(packed, g, hw, table, L: int, *,
     ms = np.empty(n, np.float64)
     st = np.empty(n, np.uint8)
     if n:
-        plan.eval_host_packed(packed, ms, st)
+        (plan.eval_host_packed if radix == 4
+         else plan.eval_host_packed3)(packed, ms, st)
     if return_status:
         return ms, st
     if n and st.max() >= N.ST_MISSING:

@@ -256,6 +256,32 @@ class Plan:
             C.byref(best) if best is not None else None, int(index_base),
             self._stream(stream)), "hs_eval_host_packed")
 
+    def packed3_ld(self) -> int:
+        """Row bytes of base-3 packed genomes (5 genes per byte)."""
+        return (self.V + 4) // 5
+
+    def eval_packed3(self, packed, makespan=None, status=None, best=None,
+                     index_base: int = 0, stream=None) -> None:
+        """hs_eval_packed3 on device tensors: packed uint8 [n, packed3_ld]."""
+        n = int(packed.shape[0])
+        N.check(self._lib.hs_eval_packed3(
+            self.handle, packed.data_ptr() if packed.numel() else None, n,
+            int(packed.stride(0)) if n > 1 else self.packed3_ld(),
+            _ptr(makespan), _ptr(status), _ptr(best), int(index_base),
+            self._stream(stream)), "hs_eval_packed3")
+
+    def eval_host_packed3(self, packed: np.ndarray, makespan=None,
+                          status=None, best: Optional[N.Best] = None,
+                          index_base: int = 0, stream=None) -> None:
+        n = packed.shape[0]
+        ld = packed.strides[0] if n > 1 else self.packed3_ld()
+        N.check(self._lib.hs_eval_host_packed3(
+            self.handle, packed.ctypes.data if n else None, n, ld,
+            makespan.ctypes.data if makespan is not None else None,
+            status.ctypes.data if status is not None else None,
+            C.byref(best) if best is not None else None, int(index_base),
+            self._stream(stream)), "hs_eval_host_packed3")
+
     def eval_gen(self, mode: int, seed: int, first: int, n: int,
                  template=None, group=None, n_groups: int = 0,
                  makespan=None, status=None, genes_out=None, best=None,

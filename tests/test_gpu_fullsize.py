@@ -108,3 +108,8 @@ def test_host_and_packed_paths(full):
     hm2 = np.empty(n, np.float64)
     plan.eval_host_packed(packed, hm2, None, hb)
     assert np.array_equal(hm2.view(np.uint64), want.view(np.uint64))
+    hm3 = np.empty(n, np.float64)
+    hb3 = N.Best()
+    plan.eval_host_packed3(hs.pack_genes3(rows), hm3, None, hb3)
+    assert np.array_equal(hm3.view(np.uint64), want.view(np.uint64))
+    assert (hb3.cost, hb3.index) == O.argmin_first(want)

@@ -227,12 +227,24 @@ def test_packed_genomes(name, oracle_lib):
         genes[0, -1] = 3  # out of range for K = 3 -> GraphError status
         want, wst = CTables(tb).fitness(oracle_lib, genes, threads=8)
         packed = hs.pack_genes(genes)
-        for arg in (packed, torch.from_numpy(packed).cuda()):
-            ms, st = hs.fitness_batch_packed(arg, g, hw, t, 1,
-                                             return_status=True)
-            ms = ms.cpu().numpy() if hasattr(ms, "cpu") else ms
-            st = st.cpu().numpy() if hasattr(st, "cpu") else st
-            assert np.array_equal(st, wst)
-            ok = wst == 0
-            assert np.array_equal(ms[ok].view(np.uint64),
-                                  want[ok].view(np.uint64))
+        # base-3: byte 255 decodes to digits 0,1,1,0,3 (out of range)
+        genes3 = genes.copy()
+        genes3[0, -1] = 2
+        genes3[0, :5] = (0, 1, 1, 0, 3)
+        want3, wst3 = CTables(tb).fitness(oracle_lib, genes3, threads=8)
+        g3 = genes3.copy()
+        g3[0, 4] = 0
+        packed3 = hs.pack_genes3(g3)
+        packed3[0, 0] = 255
+        for radix, pk, w, ws in ((4, packed, want, wst),
+                                 (3, packed3, want3, wst3)):
+            for arg in (pk, torch.from_numpy(pk).cuda()):
+                ms, st = hs.fitness_batch_packed(arg, g, hw, t, 1,
+                                                 return_status=True,
+                                                 radix=radix)
+                ms = ms.cpu().numpy() if hasattr(ms, "cpu") else ms
+                st = st.cpu().numpy() if hasattr(st, "cpu") else st
+                assert np.array_equal(st, ws)
+                ok = ws == 0
+                assert np.array_equal(ms[ok].view(np.uint64),
+                                      w[ok].view(np.uint64))

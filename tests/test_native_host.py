@@ -22,7 +22,7 @@ def test_header_symbols_exported():
     lib = _native.load()
     with open(os.path.join(ROOT, "include", "hetsched_b200.h")) as f:
         text = f.read()
-    declared = set(re.findall(r"\b(hs_[a-z_]+)\s*\(", text))
+    declared = set(re.findall(r"\b(hs_[a-z_0-9]+)\s*\(", text))
     assert declared == set(_native.exported_symbols())
     for name in declared:
         assert hasattr(lib, name), name
@@ -99,3 +99,22 @@ def test_batched_options_match_reference_enumeration():
         want = [(s, tuple(sorted(inst.dev_ids)[k] for k in dv))
                 for s, dv in B.options(inst, e["L"])]
         assert hs.batched_options(g, hw, t, e["L"]) == want
+
+
+def test_pack_genes_layouts():
+    """2-bit and base-3 packings decode back to the genes (the kernels'
+    expansion restated in numpy)."""
+    rng = np.random.default_rng(7)
+    for V in (1, 5, 32, 202, 1002):
+        genes = rng.integers(3, size=(17, V), dtype=np.uint8)
+        p3 = hs.pack_genes3(genes)
+        assert p3.shape == (17, (V + 4) // 5)
+        b = p3.astype(np.int64)
+        digits = np.stack([(b // 3 ** d) % 3 for d in range(5)], axis=2)
+        assert np.array_equal(digits.reshape(17, -1)[:, :V], genes)
+        p2 = hs.pack_genes(genes)
+        assert p2.shape[1] % 4 == 0 and p2.shape[1] * 4 >= V
+        d2 = np.stack([(p2 >> (2 * j)) & 3 for j in range(4)], axis=2)
+        assert np.array_equal(d2.reshape(17, -1)[:, :V], genes)
+    with pytest.raises(hs.GraphError):
+        hs.pack_genes3(np.full((1, 4), 3, np.uint8))
