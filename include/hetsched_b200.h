@@ -178,6 +178,33 @@ int hs_eval_host_packed3(const hs_plan *plan, const uint8_t *h_packed, int64_t n
                          int64_t ld, double *h_makespan, uint8_t *h_status,
                          hs_best *h_best, int64_t index_base, void *stream);
 
+/* The whole (1+1) EA accept chain in one launch (replaces the loop of
+ * heuristics.py:302-334 around fitness). Child c (0 <= c < budget) is the
+ * current parent with genes d_mpos[q] := d_mval[q] for q in
+ * [d_moff[c], d_moff[c+1]) -- the mutation stream does not depend on
+ * fitness, so the caller draws it up front; a child is accepted when its
+ * fitness <= the current one (:328). d_parent [V] holds the start genome
+ * (fitness cur_fit) and receives the final one; d_fit[0] = final fitness;
+ * d_info = {accepted, rounds, first child whose evaluation raised (-1 if
+ * none; the chain stops there as the reference's does), its status}. */
+int hs_ea_run(const hs_plan *plan, uint8_t *d_parent, double cur_fit,
+              const int32_t *d_moff, const int32_t *d_mpos, const uint8_t *d_mval,
+              int32_t budget, double *d_fit, int32_t *d_info, void *stream);
+
+/* Simulated annealing (heuristics.py:259-299) in one launch, resumable.
+ * All state lives in device buffers (in/out): d_genes [V] current genome,
+ * d_best [V] best-ever genome, d_rng = numpy PCG64 {state lo, state hi,
+ * inc lo, inc hi}, d_buf = {has_uint32, uinteger}, d_f = {cur_fit,
+ * best_fit, temp, -, -}, d_istate = {step, k (speculation window, start
+ * 8), stop, status, pos, new}. Runs steps until `budget`; stop = 0 done,
+ * 2 a fitness evaluation raised (status = its code; GraphError), 3 the
+ * Metropolis test at this step is within a few ulp of the device exp():
+ * the caller decides it with the host exp (u = d_f[4], candidate fitness
+ * d_f[3], move pos/new), applies it and calls again. */
+int hs_sa_run(const hs_plan *plan, uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng,
+              uint32_t *d_buf, double *d_f, int32_t *d_istate, double alpha,
+              int32_t n_dev, int32_t budget, int32_t window, void *stream);
+
 /* On-device candidates: candidate c in [first, first+n) has genes
  * oracle/hs_oracle.py::gen_genes(seed, c). Optional d_genes_out [n x V]. */
 int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,

@@ -341,6 +341,111 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     return HS_OK;
 }
 
+// K9 / K10 setup: the evaluator parameters of one CTA of ds->T lanes (AOT
+// body); `ends_g` receives the global slot tier's scratch when needed.
+int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalParams &a,
+                      Scratch &ends_g, cudaStream_t stream) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    const hs::Plan &p = plan->p;
+    if (p.batched) return set_err(HS_EINVAL, "the search kernels run on non-batched plans");
+    const hs::DevState *ds = nullptr;
+    std::string err;
+    int rc = hs::get_dev_state(p, &ds, &err);
+    if (rc) return set_err(rc, err);
+    if (ds->lanes == 0)
+        return set_err(HS_EINVAL, "graph too large for the shared-memory evaluator");
+    *dsp = ds;
+    a.blob = ds->blob;
+    a.lay = p.lay;
+    a.eval_bytes = p.lay.eval_bytes;
+    a.V = p.V;
+    a.K = p.K;
+    a.gene_range = p.K;
+    a.n_opt = p.n_opt;
+    a.P = p.P;
+    a.n_cls = p.n_cls;
+    a.flags = flags_of(p);
+    a.plan_smem = ds->plan_smem ? 1 : 0;
+    a.lanes = ds->lanes;
+    a.ld_s = p.pref_ld();
+    a.slots = p.live_slots;
+    a.smem_tile = ds->smem_tile;
+    a.smem_ends = ds->smem_ends;
+    a.smem_kstate = ds->smem_kstate;
+    ends_g.s = stream;
+    if (ds->ends_global) {
+        a.ends_g_cta = int64_t(p.live_slots) * ds->lanes;
+        CK(cudaMallocAsync(&ends_g.ptr, size_t(a.ends_g_cta) * 8, stream));
+        a.ends_g = static_cast<double *>(ends_g.ptr);
+    }
+    return HS_OK;
+}
+
+int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *moff,
+           const int32_t *mpos, const uint8_t *mval, int32_t budget, double *out_fit,
+           int32_t *info, cudaStream_t stream) {
+    if (budget < 0 || !parent || !out_fit || !info || (budget > 0 && !moff))
+        return set_err(HS_EINVAL, "bad EA arguments");
+    const hs::DevState *ds = nullptr;
+    hs::EvalParams a{};
+    Scratch ends_g;
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream);
+    if (rc) return rc;
+    std::string err;
+    hs::EaParams e{};
+    e.parent = parent;
+    e.cur_fit = cur_fit;
+    e.moff = moff;
+    e.mpos = mpos;
+    e.mval = mval;
+    e.budget = budget;
+    e.out_fit = out_fit;
+    e.info = info;
+    CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));
+    rc = hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    if (rc) return set_err(rc, err);
+    return HS_OK;
+}
+
+int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
+           uint32_t *buf, double *f, int32_t *istate, double alpha, int32_t n_dev,
+           int32_t budget, int32_t window, cudaStream_t stream) {
+    if (!genes || !best || !rng || !buf || !f || !istate || n_dev < 1 || n_dev > 256 ||
+        budget < 0 || window < 1)
+        return set_err(HS_EINVAL, "bad SA arguments");
+    const hs::DevState *ds = nullptr;
+    hs::EvalParams a{};
+    Scratch ends_g;
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream);
+    if (rc) return rc;
+    if (n_dev != plan->p.K) return set_err(HS_EINVAL, "n_dev != number of devices");
+    std::string err;
+    hs::SaParams e{};
+    e.window = std::min(window, ds->lanes);
+    Scratch spec;
+    spec.s = stream;
+    CK(cudaMallocAsync(&spec.ptr, size_t(e.window) * 16 + 64, stream));
+    uint8_t *sp = static_cast<uint8_t *>(spec.ptr);
+    e.sfit = reinterpret_cast<double *>(sp);
+    e.spos = reinterpret_cast<int32_t *>(sp + size_t(e.window) * 8);
+    e.snew = sp + size_t(e.window) * 12;
+    e.sst = sp + size_t(e.window) * 13;
+    e.genes = genes;
+    e.best = best;
+    e.rng = rng;
+    e.buf = buf;
+    e.f = f;
+    e.istate = istate;
+    e.alpha = alpha;
+    e.n_dev = n_dev;
+    e.budget = budget;
+    const char *hx = getenv("HS_SA_HOST_EXP");
+    e.host_exp = hx && atoi(hx) ? 1 : 0;
+    rc = hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    if (rc) return set_err(rc, err);
+    return HS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -705,6 +810,20 @@ int hs_eval_host_packed3(const hs_plan *plan, const uint8_t *h_packed, int64_t n
                          hs_best *h_best, int64_t index_base, void *stream) {
     return eval_host_impl(plan, h_packed, n, ld, h_makespan, h_status, h_best,
                           index_base, stream, 2);
+}
+
+int hs_ea_run(const hs_plan *plan, uint8_t *d_parent, double cur_fit,
+              const int32_t *d_moff, const int32_t *d_mpos, const uint8_t *d_mval,
+              int32_t budget, double *d_fit, int32_t *d_info, void *stream) {
+    return run_ea(plan, d_parent, cur_fit, d_moff, d_mpos, d_mval, budget, d_fit, d_info,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int hs_sa_run(const hs_plan *plan, uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng,
+              uint32_t *d_buf, double *d_f, int32_t *d_istate, double alpha,
+              int32_t n_dev, int32_t budget, int32_t window, void *stream) {
+    return run_sa(plan, d_genes, d_best, d_rng, d_buf, d_f, d_istate, alpha, n_dev, budget,
+                  window, static_cast<cudaStream_t>(stream));
 }
 
 int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,

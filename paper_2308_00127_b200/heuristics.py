@@ -468,9 +468,63 @@ def _fit_rows(plan: Plan, rows: np.ndarray) -> np.ndarray:
     return ms
 
 
+_M64 = (1 << 64) - 1
+
+
+def _sa_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
+                     best_fit: float, temp: float, alpha: float, budget: int,
+                     n_dev: int, window: int):
+    """The whole annealing run in device launches (hs_sa_run, K10): the
+    generator's PCG64 state goes to the device and comes back, so `gen` ends
+    where the reference's would. Returns (best genes, best fitness)."""
+    import torch
+    dev = torch.device("cuda")
+    bs = gen.bit_generator.state
+    s, inc = int(bs["state"]["state"]), int(bs["state"]["inc"])
+    words = [s & _M64, s >> 64, inc & _M64, inc >> 64]
+    rng = torch.tensor(np.array(words, np.uint64).view(np.int64), device=dev)
+    buf = torch.tensor(np.array([bs["has_uint32"], bs["uinteger"]],
+                                np.uint32).view(np.int32), device=dev)
+    f = torch.tensor([cur_fit, best_fit, temp, 0.0, 0.0],
+                     dtype=torch.float64, device=dev)
+    ist = torch.tensor([0, 8, 0, 0, 0, 0], dtype=torch.int32, device=dev)
+    d_genes = torch.from_numpy(genes.copy()).to(dev)
+    d_best = torch.from_numpy(genes.copy()).to(dev)
+    while True:
+        plan.sa_run(d_genes, d_best, rng, buf, f, ist, alpha, n_dev, budget,
+                    window)
+        iv = ist.cpu().numpy()
+        if iv[2] == 2:
+            _raise_status(int(iv[3]))
+        if iv[2] != 3:
+            break
+        # Metropolis too close to call on the device: CPython's exp decides
+        fv = f.cpu().numpy()
+        cur, bestf, tmp, cand, u = (float(x) for x in fv)
+        pos, new = int(iv[4]), int(iv[5])
+        acc = u < math.exp(-(cand - cur) / tmp)
+        if acc:
+            d_genes[pos] = new
+            cur = cand
+            if cand < bestf:
+                bestf = cand
+                d_best.copy_(d_genes)
+        f.copy_(torch.tensor([cur, bestf, tmp * alpha, 0.0, 0.0],
+                             dtype=torch.float64))
+        ist.copy_(torch.tensor([int(iv[0]) + 1, 8, 0, 0, 0, 0],
+                               dtype=torch.int32))
+    w = rng.cpu().numpy().view(np.uint64)
+    b = buf.cpu().numpy().view(np.uint32)
+    bs["state"]["state"] = int(w[0]) | (int(w[1]) << 64)
+    bs["has_uint32"], bs["uinteger"] = int(b[0]), int(b[1])
+    gen.bit_generator.state = bs
+    return d_best.cpu().numpy(), float(f[1].item())
+
+
 def simulated_annealing(g, hw, table, L: int, seed: int = 0,
                         budget: int = 2000, t0_fraction: float = 0.1,
-                        alpha: float = 0.995, window: int = 64) -> Schedule:
+                        alpha: float = 0.995, window: int = 64,
+                        device_chain: bool = True) -> Schedule:
     """Single-gene reassignment, geometric cooling, Metropolis acceptance,
     greedy start, best-ever genome decoded (heuristics.py:259-299).
 
@@ -478,7 +532,9 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     the candidates of the next `window` steps for every stream position the
     run can reach if those steps are rejected (a step draws ``random()`` only
     when the candidate is finite and worse, so positions branch); the host
-    replays the steps against the batch until the first acceptance.
+    replays the steps against the batch until the first acceptance. With
+    `device_chain` the same speculation and replay run inside one kernel
+    launch (K10, hs_sa_run) with numpy's PCG64 restated on the device.
     """
     gen = np.random.default_rng(seed)
     start = greedy(g, hw, table, L)
@@ -492,6 +548,11 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     plan = get_plan(g, hw, table, L)
     genes = np.array(cur.genes, np.uint8)
     step = 0
+    if device_chain and V and budget > 0:
+        best, best_fit = _sa_device_chain(plan, gen, genes, cur_fit, best_fit,
+                                          temp, alpha, budget, n_dev,
+                                          max(window, 128))
+        step = budget
     k = max(1, min(window, 8))
     while step < budget:
         k = min(k, budget - step)
@@ -566,14 +627,51 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     return out
 
 
+def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
+                     budget: int, V: int, n_dev: int, p: float):
+    """Every child's mutations drawn up front, then the whole accept chain
+    in one kernel launch (hs_ea_run, K9). Returns (genes, fitness)."""
+    import torch
+    need = budget * (V + 2) + 64
+    while True:
+        S, words, st = R.peek_words(gen, need)
+        try:
+            muts = R.ea_mutations(S, words, st, budget, V, n_dev, p)
+            break
+        except IndexError:
+            need *= 2
+    counts = np.fromiter((len(m[0]) for m in muts), np.int32, budget)
+    moff = np.zeros(budget + 1, np.int32)
+    np.cumsum(counts, out=moff[1:])
+    flat = [pv for m in muts for pv in m[0]]
+    mpos = np.fromiter((pv[0] for pv in flat), np.int32, len(flat))
+    mval = np.fromiter((pv[1] for pv in flat), np.uint8, len(flat))
+    dev = torch.device("cuda")
+    d_parent = torch.from_numpy(genes.copy()).to(dev)
+    d_moff = torch.from_numpy(moff).to(dev)
+    d_mpos = torch.from_numpy(mpos).to(dev)
+    d_mval = torch.from_numpy(mval).to(dev)
+    d_fit = torch.empty(1, dtype=torch.float64, device=dev)
+    d_info = torch.empty(4, dtype=torch.int32, device=dev)
+    plan.ea_run(d_parent, cur_fit, d_moff, d_mpos, d_mval, budget, d_fit,
+                d_info)
+    info = d_info.cpu().numpy()
+    if info[2] >= 0:
+        _raise_status(int(info[3]))
+    R.commit(gen, muts[-1][1])
+    return d_parent.cpu().numpy(), float(d_fit.cpu()[0])
+
+
 def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
-                    biased: bool = True, window: int = 256) -> Schedule:
+                    biased: bool = True, window: int = 256,
+                    device_chain: bool = True) -> Schedule:
     """(1+1) EA: each gene mutated with probability 1/|V|, accept when not
     worse; biased start = MET, unbiased = uniform genes
     (heuristics.py:302-334). The mutation stream does not depend on fitness,
-    so `window` children are drawn ahead and evaluated in one GPU batch;
-    an acceptance re-bases the remaining children (same trajectory as the
-    reference)."""
+    so every child's mutation list is drawn ahead. With `device_chain` the
+    whole accept chain runs in one kernel launch (K9, hs_ea_run); otherwise
+    `window` children are evaluated per GPU batch and an acceptance re-bases
+    the remaining children. Either way the trajectory is the reference's."""
     gen = np.random.default_rng(seed)
     order = tuple(bfs_topological_order(g))
     n_dev = len(hw.devices)
@@ -590,6 +688,10 @@ def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
     genes = np.array(cur.genes, np.uint8)
     plan = get_plan(g, hw, table, L) if V else None
     step = 0
+    if device_chain and V and budget > 0:
+        genes, cur_fit = _ea_device_chain(plan, gen, genes, cur_fit, budget,
+                                          V, n_dev, p)
+        step = budget
     while step < budget:
         k = min(window, budget - step)
         S, words, st = R.peek_words(gen, k * (V + 2) + 64)

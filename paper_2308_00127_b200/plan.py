@@ -256,6 +256,27 @@ class Plan:
             C.byref(best) if best is not None else None, int(index_base),
             self._stream(stream)), "hs_eval_host_packed")
 
+    def ea_run(self, parent, cur_fit: float, moff, mpos, mval, budget: int,
+               fit, info, stream=None) -> None:
+        """hs_ea_run (K9) on device tensors: parent uint8 [V] (in/out),
+        moff int32 [budget+1], mpos int32, mval uint8, fit f64 [1],
+        info int32 [4]."""
+        N.check(self._lib.hs_ea_run(
+            self.handle, _ptr(parent), float(cur_fit), _ptr(moff),
+            _ptr(mpos) if mpos.numel() else None,
+            _ptr(mval) if mval.numel() else None, int(budget), _ptr(fit),
+            _ptr(info), self._stream(stream)), "hs_ea_run")
+
+    def sa_run(self, genes, best, rng, buf, f, istate, alpha: float,
+               n_dev: int, budget: int, window: int, stream=None) -> None:
+        """hs_sa_run (K10) on device tensors (all state in/out): genes /
+        best uint8 [V], rng int64 [4] (PCG64 words), buf int32 [2], f f64
+        [5], istate int32 [6]."""
+        N.check(self._lib.hs_sa_run(
+            self.handle, _ptr(genes), _ptr(best), _ptr(rng), _ptr(buf),
+            _ptr(f), _ptr(istate), float(alpha), int(n_dev), int(budget),
+            int(window), self._stream(stream)), "hs_sa_run")
+
     def packed3_ld(self) -> int:
         """Row bytes of base-3 packed genomes (5 genes per byte)."""
         return (self.V + 4) // 5

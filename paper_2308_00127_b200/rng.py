@@ -18,6 +18,8 @@ this against numpy itself over many seeds and ranges.
 """
 from __future__ import annotations
 
+from bisect import bisect_left
+
 import numpy as np
 
 M32 = 0xFFFFFFFF
@@ -30,18 +32,24 @@ class RawStream:
     __slots__ = ("w",)
 
     def __init__(self, words: np.ndarray):
-        self.w = [int(x) for x in words]
+        # numpy words, converted on access: the EA peeks ~V words per step
+        # but reads only the few that hit
+        self.w = np.asarray(words, np.uint64)
 
     def next32(self, st):
         i, has, u = st
         if has:
             return u, (i, 0, 0)
-        x = self.w[i]
+        if i >= len(self.w):
+            raise IndexError("peek window exhausted")
+        x = int(self.w[i])
         return x & M32, (i + 1, 1, x >> 32)
 
     def next64(self, st):
         i, has, u = st
-        return self.w[i], (i + 1, has, u)
+        if i >= len(self.w):
+            raise IndexError("peek window exhausted")
+        return int(self.w[i]), (i + 1, has, u)
 
     def random(self, st):
         x, st = self.next64(st)
@@ -97,8 +105,8 @@ def ea_mutations(S: RawStream, words: np.ndarray, st, steps: int, V: int,
     peeked words run out (the caller shortens its window)."""
     W = len(words)
     u = (words >> np.uint64(11)).astype(np.float64) * _D53
-    idx = np.where(u < p, np.arange(W), W)
-    nxt = np.minimum.accumulate(idx[::-1])[::-1].tolist()
+    hits = np.flatnonzero(u < p).tolist()  # word indices with random() < p
+    hits.append(W)
     out = []
     i, has, c = st
     for _ in range(steps):
@@ -108,7 +116,7 @@ def ea_mutations(S: RawStream, words: np.ndarray, st, steps: int, V: int,
             rem = V - pos
             if i + rem > W:
                 raise IndexError("peek window exhausted")
-            j = nxt[i]
+            j = hits[bisect_left(hits, i)]  # first hit at or after i
             if j >= i + rem:
                 i += rem
                 break

@@ -62,9 +62,56 @@ def test_search_trajectories(idx):
 def test_sa_window_sizes_agree():
     e = [x for x in _entries() if x["name"] == "ws30"][0]
     g, hw, t = hs.load_instance(e)
-    a = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=1)
-    b = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=128)
+    a = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=1,
+                               device_chain=False)
+    b = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400, window=128,
+                               device_chain=False)
+    b2 = hs.simulated_annealing(g, hw, t, 1, seed=4, budget=400)
+    assert a == b == b2
+    c = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=1,
+                           device_chain=False)
+    d = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=97,
+                           device_chain=False)
+    e2 = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300)
+    assert c == d == e2
+
+
+@pytest.mark.parametrize("name", ["ws_stack_10x20", "rn50f", "tf96", "ws1000"])
+def test_ea_device_chain_matches_windows(name):
+    """K9 (whole accept chain in one launch) == windowed GPU batches on
+    larger graphs and budgets, biased and unbiased starts."""
+    from conftest import instance_doc
+    g, hw, t = hs.load_instance(instance_doc(name))
+    for biased in (True, False):
+        for seed in (0, 3):
+            a = hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=1500,
+                                   biased=biased, device_chain=False)
+            b = hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=1500,
+                                   biased=biased)
+            assert a == b, (name, biased, seed)
+
+
+@pytest.mark.parametrize("name", ["ws_stack_10x20", "rn50f", "tf96", "ws1000"])
+def test_sa_device_chain_matches_windows(name):
+    """K10 (speculative SA with PCG64 on the device, one launch) == the
+    host-replayed windows."""
+    from conftest import instance_doc
+    g, hw, t = hs.load_instance(instance_doc(name))
+    budget = 600 if name == "ws1000" else 1500
+    for seed in (0, 3):
+        a = hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=budget,
+                                   device_chain=False)
+        b = hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=budget)
+        assert a == b, (name, seed)
+
+
+def test_sa_host_exp_path(monkeypatch):
+    """Every Metropolis test handed back to the host (the rare too-close-
+    to-call path of K10) still gives the reference trajectory."""
+    from conftest import instance_doc
+    g, hw, t = hs.load_instance(instance_doc("ws30"))
+    a = hs.simulated_annealing(g, hw, t, 1, seed=2, budget=300,
+                               device_chain=False)
+    monkeypatch.setenv("HS_SA_HOST_EXP", "1")
+    b = hs.simulated_annealing(g, hw, t, 1, seed=2, budget=300)
     assert a == b
-    c = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=1)
-    d = hs.one_plus_one_ea(g, hw, t, 1, seed=4, budget=300, window=97)
-    assert c == d
