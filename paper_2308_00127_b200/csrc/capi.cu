@@ -344,7 +344,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
 // K9 / K10 setup: the evaluator parameters of one CTA of ds->T lanes (AOT
 // body); `ends_g` receives the global slot tier's scratch when needed.
 int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalParams &a,
-                      Scratch &ends_g, cudaStream_t stream) {
+                      Scratch &ends_g, cudaStream_t stream, const hs::JitModule **jmp) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
     const hs::Plan &p = plan->p;
     if (p.batched) return set_err(HS_EINVAL, "the search kernels run on non-batched plans");
@@ -372,9 +372,23 @@ int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalPar
     a.smem_tile = ds->smem_tile;
     a.smem_ends = ds->smem_ends;
     a.smem_kstate = ds->smem_kstate;
+    // the graph-specialised module's search kernels when it has them
+    const hs::JitModule *jm = hs::find_jit(p, ds->device);
+    if (jm && (!jm->kern_sa || !jm->kern_ea)) jm = nullptr;
+    if (const char *v = getenv("HS_SEARCH_AOT"))
+        if (atoi(v)) jm = nullptr;
+    *jmp = jm;
+    if (jm) {
+        a.sanitize = 1;
+        a.lanes = jm->lanes;
+        a.slots = jm->slots;
+        a.smem_tile = jm->smem_tile;
+        a.smem_ends = jm->smem_ends;
+        a.smem_kstate = jm->smem_kstate;
+    }
     ends_g.s = stream;
-    if (ds->ends_global) {
-        a.ends_g_cta = int64_t(p.live_slots) * ds->lanes;
+    if (jm ? jm->ends_global : ds->ends_global) {
+        a.ends_g_cta = int64_t(a.slots) * a.lanes;
         CK(cudaMallocAsync(&ends_g.ptr, size_t(a.ends_g_cta) * 8, stream));
         a.ends_g = static_cast<double *>(ends_g.ptr);
     }
@@ -387,9 +401,10 @@ int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *
     if (budget < 0 || !parent || !out_fit || !info || (budget > 0 && !moff))
         return set_err(HS_EINVAL, "bad EA arguments");
     const hs::DevState *ds = nullptr;
+    const hs::JitModule *jm = nullptr;
     hs::EvalParams a{};
     Scratch ends_g;
-    int rc = single_cta_params(plan, &ds, a, ends_g, stream);
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm);
     if (rc) return rc;
     std::string err;
     hs::EaParams e{};
@@ -402,7 +417,8 @@ int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *
     e.out_fit = out_fit;
     e.info = info;
     CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));
-    rc = hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    rc = jm ? hs::jit_launch_search(*jm, 2, a, &e, stream, &err)
+            : hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err);
     if (rc) return set_err(rc, err);
     return HS_OK;
 }
@@ -414,14 +430,15 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
         budget < 0 || window < 1)
         return set_err(HS_EINVAL, "bad SA arguments");
     const hs::DevState *ds = nullptr;
+    const hs::JitModule *jm = nullptr;
     hs::EvalParams a{};
     Scratch ends_g;
-    int rc = single_cta_params(plan, &ds, a, ends_g, stream);
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm);
     if (rc) return rc;
     if (n_dev != plan->p.K) return set_err(HS_EINVAL, "n_dev != number of devices");
     std::string err;
     hs::SaParams e{};
-    e.window = std::min(window, ds->lanes);
+    e.window = std::min(window, a.lanes);
     Scratch spec;
     spec.s = stream;
     CK(cudaMallocAsync(&spec.ptr, size_t(e.window) * 16 + 64, stream));
@@ -432,7 +449,7 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.sst = sp + size_t(e.window) * 13;
     e.genes = genes;
     e.best = best;
-    e.rng = rng;
+    e.rng = reinterpret_cast<hs_u64 *>(rng);
     e.buf = buf;
     e.f = f;
     e.istate = istate;
@@ -441,7 +458,8 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.budget = budget;
     const char *hx = getenv("HS_SA_HOST_EXP");
     e.host_exp = hx && atoi(hx) ? 1 : 0;
-    rc = hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    rc = jm ? hs::jit_launch_search(*jm, 1, a, &e, stream, &err)
+            : hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err);
     if (rc) return set_err(rc, err);
     return HS_OK;
 }

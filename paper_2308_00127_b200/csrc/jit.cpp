@@ -720,7 +720,8 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         s += "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg, tb, dg);\n";
     }
     s += "  }\n};\n";
-    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
+    s += "template <bool TRACE, int MODE>\n__device__ __forceinline__ void jit_main("
+         "const EvalParams &a, const SaParams *sa, const EaParams *ea) {\n"
          "  extern __shared__ __align__(16) hs_u8 smem[];\n";
     if (l.dur) s += stage(l.dur_off, "dur", int64_t(V) * K * 8);
     if (l.cls) {
@@ -747,7 +748,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         s += "  body.tb = tm_base_s + ((((threadIdx.x >> 5) & 3u) * 32u) << 16) + (threadIdx.x >> 7) * " +
              std::to_string(o.tm_cols) + "u;\n";
     }
-    s += "  eval_tiles(a, smem, body);\n";
+    s += "  if constexpr (MODE == 0) eval_tiles(a, smem, body);\n"
+         "  else if constexpr (MODE == 1) sa_chain(a, *sa, smem, body);\n"
+         "  else ea_chain(a, *ea, smem, body);\n";
     if (o.tmem)
         s += "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
              "  __syncthreads();\n"
@@ -759,10 +762,23 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
     s += "}\n";
     std::snprintf(buf, sizeof buf,
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
-                  "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
+                  "hs_jit_eval(const EvalParams a) { jit_main<false, 0>(a, nullptr, nullptr); }\n"
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
-                  "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n", T, T);
+                  "hs_jit_trace(const EvalParams a) { jit_main<true, 0>(a, nullptr, nullptr); }\n",
+                  T, T);
     s += buf;
+    if (jit_search_ok(p)) {
+        // single-CTA search drivers (SA K10, EA K9) over the specialised body
+        std::snprintf(buf, sizeof buf,
+                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                      "hs_jit_sa(const EvalParams a, const SaParams e) "
+                      "{ jit_main<false, 1>(a, &e, nullptr); }\n"
+                      "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                      "hs_jit_ea(const EvalParams a, const EaParams e) "
+                      "{ jit_main<false, 2>(a, nullptr, &e); }\n",
+                      T, T);
+        s += buf;
+    }
     if (greg) {
         // Direct-load kernel: no genome tile and no CTA barrier per tile.
         // Each thread reads its own row from global memory (L1-cached
@@ -827,6 +843,14 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
              "  if (a.best) reduce_best(bc, bi, a.partial, a.ticket, a.best);\n}\n";
     }
     return next;
+}
+
+bool jit_search_ok(const Plan &p) {
+    // the search kernels double the inlined straight-line code: only where
+    // NVRTC stays fast
+    if (const char *v = getenv("HS_JIT_SEARCH"))
+        if (!atoi(v)) return false;
+    return p.V <= 512 && !p.batched;
 }
 
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
@@ -968,6 +992,16 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     if (e == cudaSuccess)
         e = cudaKernelSetAttributeForDevice(
             m->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
+    if (e == cudaSuccess && jit_search_ok(p)) {
+        e = cudaLibraryGetKernel(&m->kern_sa, m->lib, "hs_jit_sa");
+        if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern_ea, m->lib, "hs_jit_ea");
+        if (e == cudaSuccess)
+            e = cudaKernelSetAttributeForDevice(
+                m->kern_sa, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
+        if (e == cudaSuccess)
+            e = cudaKernelSetAttributeForDevice(
+                m->kern_ea, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
+    }
     if (e == cudaSuccess && o.genes_reg && p.K <= 4) {
         m->smem_direct = size_t(m->smem_tile);
         e = cudaLibraryGetKernel(&m->kern_direct, m->lib, "hs_jit_direct");
@@ -1009,6 +1043,22 @@ void jit_free(JitModule *m) {
 bool jit_direct_ok(const JitModule &m, const hsk::EvalParams &a) {
     return m.kern_direct && !a.starts && !a.gen && !a.packed && a.ld % 4 == 0 &&
            (reinterpret_cast<uintptr_t>(a.genes) & 3) == 0;
+}
+
+int jit_launch_search(const JitModule &m, int mode, const hsk::EvalParams &a,
+                      const void *ps, cudaStream_t stream, std::string *err) {
+    const cudaKernel_t k = mode == 1 ? m.kern_sa : m.kern_ea;
+    if (!k) {
+        if (err) *err = "specialised module has no search kernels";
+        return HS_EINVAL;
+    }
+    void *args[] = {(void *)&a, const_cast<void *>(ps)};
+    cudaError_t e = cudaLaunchKernel((const void *)k, dim3(1), dim3(m.T), args, m.smem, stream);
+    if (e != cudaSuccess) {
+        if (err) *err = std::string("specialised search launch: ") + cudaGetErrorString(e);
+        return HS_ECUDA;
+    }
+    return HS_OK;
 }
 
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid, cudaStream_t stream,

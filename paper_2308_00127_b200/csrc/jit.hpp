@@ -45,6 +45,7 @@ struct JitModule {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t kern = nullptr, kern_trace = nullptr;
     cudaKernel_t kern_direct = nullptr;  // genes from global into registers
+    cudaKernel_t kern_sa = nullptr, kern_ea = nullptr;  // single-CTA search
     size_t smem_direct = 0;
     bool ends_global = false;  // end-time slots in global memory
     bool tmem = false;         // end-time slots in tensor memory
@@ -58,6 +59,7 @@ struct JitModule {
 };
 
 bool jit_eligible(const Plan &p);
+bool jit_search_ok(const Plan &p);
 // Emits the kernel for T lanes; returns the number of shared-memory slots.
 int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src);
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err);
@@ -66,5 +68,8 @@ void jit_free(JitModule *m);
 bool jit_direct_ok(const JitModule &m, const hsk::EvalParams &a);
 int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid,
                cudaStream_t stream, std::string *err);
+// one CTA of the SA (mode 1) or EA (mode 2) search kernel; `ps` -> params
+int jit_launch_search(const JitModule &m, int mode, const hsk::EvalParams &a,
+                      const void *ps, cudaStream_t stream, std::string *err);
 
 }  // namespace hs

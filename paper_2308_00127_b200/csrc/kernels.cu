@@ -347,53 +347,6 @@ __device__ __forceinline__ void single_cta_body(const EvalParams &a, hs_u8 *smem
     __syncthreads();
 }
 
-// numpy Generator(PCG64) on the device (oracle restatement: rng.py): the
-// 128-bit LCG step then the XSL-RR output; 32-bit draws take the buffered
-// upper half of the previous word; integers(high) is Lemire's method on
-// 32-bit draws; random() = (word >> 11) * 2^-53.
-struct Pcg64 {
-    hs_u64 slo, shi, ilo, ihi;
-    hs_u32 has, cached;
-    __device__ __forceinline__ hs_u64 next64() {
-        const hs_u64 ml = 4865540595714422341ull, mh = 2549297995355413924ull;
-        const hs_u64 lo = slo * ml;
-        hs_u64 hi = __umul64hi(slo, ml) + slo * mh + shi * ml;
-        const hs_u64 lo2 = lo + ilo;
-        hi += ihi + (lo2 < lo ? 1ull : 0ull);
-        slo = lo2;
-        shi = hi;
-        const hs_u64 x = hi ^ lo2;
-        const unsigned rot = (unsigned)(hi >> 58);
-        return (x >> rot) | (x << ((64u - rot) & 63u));
-    }
-    __device__ __forceinline__ hs_u32 next32() {
-        if (has) {
-            has = 0;
-            return cached;
-        }
-        const hs_u64 x = next64();
-        has = 1;
-        cached = (hs_u32)(x >> 32);
-        return (hs_u32)x;
-    }
-    __device__ __forceinline__ int integers(hs_u32 high) {
-        if (high <= 1) return 0;
-        hs_u64 m = (hs_u64)next32() * high;
-        hs_u32 left = (hs_u32)m;
-        if (left < high) {
-            const hs_u32 thr = (0xFFFFFFFFu - (high - 1)) % high;
-            while (left < thr) {
-                m = (hs_u64)next32() * high;
-                left = (hs_u32)m;
-            }
-        }
-        return (int)(m >> 32);
-    }
-    __device__ __forceinline__ double random() {
-        return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
-    }
-};
-
 // ---------------------------------------------------------------------------
 // K10: simulated annealing (heuristics.py:259-299) in one launch. Rounds of
 // speculation: thread 0 draws the next k steps' moves assuming each is
@@ -408,126 +361,9 @@ struct Pcg64 {
 template <int KT, bool CLASS, bool FAST>
 __global__ void __launch_bounds__(512) sa_kernel(const EvalParams a, const SaParams e) {
     extern __shared__ __align__(16) hs_u8 smem[];
-    __shared__ int s_k, s_step, s_go;
     PlanBody<KT, CLASS, FAST> body;
     single_cta_body(a, smem, body);
-    const int l = threadIdx.x;
-    hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
-    hs_u8 *genes = e.genes;
-    const int V = a.V, budget = e.budget;
-    const hs_u32 nd1 = (hs_u32)(e.n_dev - 1);
-    Pcg64 r;
-    double cur = 0.0, bestf = 0.0, temp = 0.0;
-    int step = 0, stop = 0;
-    if (l == 0) {
-        r.slo = e.rng[0];
-        r.shi = e.rng[1];
-        r.ilo = e.rng[2];
-        r.ihi = e.rng[3];
-        r.has = e.buf[0];
-        r.cached = e.buf[1];
-        cur = e.f[0];
-        bestf = e.f[1];
-        temp = e.f[2];
-        step = e.istate[0];
-        s_k = e.istate[1];
-        s_step = step;
-        s_go = 1;
-    }
-    __syncthreads();
-    for (;;) {
-        const int kk = s_k, stp = s_step;
-        if (!s_go || stp >= budget) break;
-        const int n = kk < budget - stp ? kk : budget - stp;
-        if (l == 0) {  // speculative moves of the next n steps
-            Pcg64 q = r;
-            for (int i = 0; i < n; ++i) {
-                const int pos = q.integers((hs_u32)V);
-                const int old = genes[pos];
-                int nw = old;
-                if (e.n_dev > 1) {
-                    nw = q.integers(nd1);
-                    if (nw >= old) ++nw;
-                }
-                e.spos[i] = pos;
-                e.snew[i] = (hs_u8)nw;
-                (void)q.random();
-            }
-        }
-        __syncthreads();
-        for (int i = 0; i < V; ++i) row[i] = genes[i];
-        const bool valid = l < n;
-        if (valid) row[e.spos[l]] = e.snew[l];
-        double ms = 0.0;
-        int st = 0;
-        body.run(row, l, stp + l, valid, 0, ms, st);
-        if (valid) {
-            e.sfit[l] = ms;
-            e.sst[l] = (hs_u8)st;
-        }
-        __syncthreads();
-        if (l == 0) {  // replay with the real generator
-            bool acc = false;
-            for (int i = 0; i < n; ++i) {
-                const int pos = r.integers((hs_u32)V);
-                const int old = genes[pos];
-                int nw = old;
-                if (e.n_dev > 1) {
-                    nw = r.integers(nd1);
-                    if (nw >= old) ++nw;
-                }
-                const double cand = e.sfit[i];
-                if (e.sst[i] >= ST_MISSING) {  // fitness raised
-                    stop = 2;
-                    e.istate[3] = e.sst[i];
-                    break;
-                }
-                const double delta = cand - cur;
-                acc = delta <= 0.0;
-                const bool fin = isfinite(cand);
-                if (!acc && fin) {
-                    const double u = r.random();
-                    const double ex = exp(-delta / temp);
-                    if (e.host_exp || u == 0.0 || fabs(u - ex) <= ex * 0x1p-48) {
-                        stop = 3;  // too close to call against CPython's exp
-                        e.istate[4] = pos;
-                        e.istate[5] = nw;
-                        e.f[3] = cand;
-                        e.f[4] = u;
-                        break;
-                    }
-                    acc = u < ex;
-                }
-                ++step;
-                if (acc) {
-                    genes[pos] = (hs_u8)nw;
-                    cur = cand;
-                    if (cand < bestf) {
-                        bestf = cand;
-                        for (int j = 0; j < V; ++j) e.best[j] = genes[j];
-                    }
-                }
-                temp *= e.alpha;
-                if (acc || !fin) break;
-            }
-            s_k = acc ? 8 : (2 * kk < e.window ? 2 * kk : e.window);
-            s_step = step;
-            if (stop) s_go = 0;
-        }
-        __syncthreads();
-    }
-    if (l == 0) {
-        e.rng[0] = r.slo;
-        e.rng[1] = r.shi;
-        e.buf[0] = r.has;
-        e.buf[1] = r.cached;
-        e.f[0] = cur;
-        e.f[1] = bestf;
-        e.f[2] = temp;
-        e.istate[0] = step;
-        e.istate[1] = s_k;
-        e.istate[2] = stop;
-    }
+    sa_chain(a, e, smem, body);
 }
 
 // ---------------------------------------------------------------------------
@@ -544,59 +380,9 @@ __global__ void __launch_bounds__(512) sa_kernel(const EvalParams a, const SaPar
 template <int KT, bool CLASS, bool FAST>
 __global__ void __launch_bounds__(512) ea_kernel(const EvalParams a, const EaParams e) {
     extern __shared__ __align__(16) hs_u8 smem[];
-    __shared__ int s_first;
-    __shared__ double s_fit;
     PlanBody<KT, CLASS, FAST> body;
     single_cta_body(a, smem, body);
-    const int l = threadIdx.x;
-    hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
-    hs_u8 *parent = e.parent;  // [V], global; written by one lane per round
-    double cur = e.cur_fit;
-    int acc = 0, rounds = 0, err_child = -1, err_st = 0;
-    for (int j = 0; j < e.budget;) {
-        if (l == 0) s_first = a.lanes;
-        __syncthreads();  // parent / s_first of the previous round settled
-        for (int i = 0; i < a.V; ++i) row[i] = parent[i];
-        const int c = j + l;
-        const bool valid = c < e.budget;
-        if (valid)
-            for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) row[e.mpos[q]] = e.mval[q];
-        double ms = 0.0;
-        int st = 0;
-        body.run(row, l, c, valid, 0, ms, st);
-        if (valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
-        __syncthreads();
-        const int r = s_first;
-        ++rounds;
-        if (r == a.lanes) {
-            j += a.lanes;
-            continue;
-        }
-        if (l == r) {
-            if (st >= ST_MISSING) {
-                s_fit = -1.0;
-            } else {
-                for (int i = 0; i < a.V; ++i) parent[i] = row[i];
-                s_fit = ms;
-            }
-        }
-        __syncthreads();
-        if (s_fit < 0.0) {  // fitness raised: the reference stops here
-            err_child = j + r;
-            if (l == r) err_st = st;
-            break;
-        }
-        cur = s_fit;
-        ++acc;
-        j += r + 1;
-    }
-    if (err_st) e.info[3] = err_st;  // the raising lane only
-    if (l == 0) {
-        e.out_fit[0] = cur;
-        e.info[0] = acc;
-        e.info[1] = rounds;
-        e.info[2] = err_child;
-    }
+    ea_chain(a, e, smem, body);
 }
 
 // ---------------------------------------------------------------------------

@@ -16,6 +16,8 @@ using hsk::F_MEM;
 using hsk::F_MISS;
 using hsk::F_NAN;
 using hsk::F_OKL;
+using hsk::EaParams;
+using hsk::SaParams;
 
 int eval_occupancy(int kt, bool cls, int T, size_t smem, int *blocks);
 int beval_occupancy(int T, size_t smem, int *blocks);
@@ -23,36 +25,6 @@ int launch_beval(const DevState &ds, const EvalParams &p, int grid,
                  cudaStream_t stream, std::string *err);
 int launch_eval(const DevState &ds, bool cls, const EvalParams &p, int grid,
                 cudaStream_t stream, std::string *err);
-// (1+1) EA accept chain (K9): every child's mutations, drawn on the host
-struct EaParams {
-    uint8_t *parent;      // [V] in: start genome, out: final genome
-    double cur_fit;       // fitness of the start genome
-    const int32_t *moff;  // [budget + 1] CSR offsets into mpos / mval
-    const int32_t *mpos;  // mutated genome positions
-    const uint8_t *mval;  // new genes
-    int budget;
-    double *out_fit;      // [1] final fitness
-    int32_t *info;        // [4] accepted, rounds, raising child (-1), status
-};
-
-// simulated annealing (K10); all state in/out so a run can resume
-struct SaParams {
-    uint8_t *genes;    // [V] current genome (in/out)
-    uint8_t *best;     // [V] best-ever genome (in/out)
-    uint64_t *rng;     // [4] PCG64 state lo, hi, increment lo, hi (in/out)
-    uint32_t *buf;     // [2] has_uint32, cached upper half (in/out)
-    double *f;         // [5] cur, best, temp (in/out); stop 3: cand, u
-    int32_t *istate;   // [6] step, k (in/out); stop (0 done, 2 raised, 3
-                       // host decides), raised status, stop 3: pos, new
-    int32_t *spos;     // [window] speculative moves
-    uint8_t *snew;
-    double *sfit;      // [window] speculative fitness, status
-    uint8_t *sst;
-    double alpha;
-    int n_dev, budget, window;
-    int host_exp;      // test hook: hand every Metropolis test to the host
-};
-
 int launch_sa(const DevState &ds, bool cls, const EvalParams &p, const SaParams &sa,
               cudaStream_t stream, std::string *err);
 int launch_ea(const DevState &ds, bool cls, const EvalParams &p, const EaParams &ea,

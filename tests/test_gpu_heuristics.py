@@ -89,6 +89,12 @@ def test_ea_device_chain_matches_windows(name):
             b = hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=1500,
                                    biased=biased)
             assert a == b, (name, biased, seed)
+    # again through the graph-specialised module's search kernel
+    if len(g.tasks) <= 512 and hs.specialize(g, hw, t, 1) >= 0:
+        c = hs.one_plus_one_ea(g, hw, t, 1, seed=3, budget=1500, biased=False)
+        d = hs.one_plus_one_ea(g, hw, t, 1, seed=3, budget=1500, biased=False,
+                               device_chain=False)
+        assert c == d, name
 
 
 @pytest.mark.parametrize("name", ["ws_stack_10x20", "rn50f", "tf96", "ws1000"])
@@ -103,6 +109,10 @@ def test_sa_device_chain_matches_windows(name):
                                    device_chain=False)
         b = hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=budget)
         assert a == b, (name, seed)
+    # again through the graph-specialised module's search kernel
+    if len(g.tasks) <= 512 and hs.specialize(g, hw, t, 1) >= 0:
+        c = hs.simulated_annealing(g, hw, t, 1, seed=3, budget=budget)
+        assert c == a, name
 
 
 def test_sa_host_exp_path(monkeypatch):

@@ -47,6 +47,8 @@ def test_emit_and_compile(which):
         p = Plan(*hs.load_instance(instance_doc(which)), 1)
     src = p.specialized_source(64)
     assert "hs_jit_eval" in src and "hs_jit_trace" in src
+    # single-CTA search kernels (SA K10 / EA K9) for graphs up to 512 tasks
+    assert ("hs_jit_sa" in src and "hs_jit_ea" in src) == (p.V <= 512)
     rc, log = _nvrtc_compile(src)
     assert rc == 0, log[-2000:]
 
