@@ -18,6 +18,7 @@ this against numpy itself over many seeds and ranges.
 """
 from __future__ import annotations
 
+import math
 from bisect import bisect_left
 
 import numpy as np
@@ -104,9 +105,14 @@ def ea_mutations(S: RawStream, words: np.ndarray, st, steps: int, V: int,
     Returns [(mutations, state after the step)]; raises IndexError when the
     peeked words run out (the caller shortens its window)."""
     W = len(words)
-    u = (words >> np.uint64(11)).astype(np.float64) * _D53
-    hits = np.flatnonzero(u < p).tolist()  # word indices with random() < p
-    hits.append(W)
+    # random() < p  <=>  (w >> 11) * 2^-53 < p  <=>  (w >> 11) < ceil(p * 2^53)
+    # (the scalings by 2^53 are exact)  <=>  w < ceil(p * 2^53) * 2^11
+    lim = math.ceil(p * 9007199254740992.0) << 11
+    if lim >= 1 << 64:
+        hits = list(range(W))
+    else:
+        hits = np.flatnonzero(words < np.uint64(lim)).tolist()
+    hits.append(W)  # word indices with random() < p, then a sentinel
     out = []
     i, has, c = st
     for _ in range(steps):

@@ -53,3 +53,21 @@ def test_ea_mutations_match_reference_loop():
             R.commit(mirror, got[-1][1])
         assert real.bit_generator.state["state"] == \
             mirror.bit_generator.state["state"]
+
+
+def test_random_below_p_integer_threshold():
+    """ea_mutations finds random() < p hits with one integer compare per
+    raw word; it equals the float test, including words at the boundary."""
+    import math
+    for V in (1, 2, 3, 7, 32, 202, 220, 1002):
+        p = 1.0 / V
+        lim = math.ceil(p * 2.0 ** 53) << 11
+        ws = np.random.default_rng(V).integers(
+            0, 2 ** 64 - 1, size=100_000, dtype=np.uint64, endpoint=True)
+        edge = [x for x in (lim - 1, lim, lim + 1, lim - 2048, lim + 2047)
+                if 0 <= x < 2 ** 64]
+        ws = np.concatenate([ws, np.array(edge, np.uint64)])
+        want = ((ws >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) < p
+        got = (ws < np.uint64(lim)) if lim < 2 ** 64 else \
+            np.ones(len(ws), bool)
+        assert np.array_equal(want, got), V
