@@ -590,8 +590,9 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
         for r, s in enumerate(keys):
             pos, new, _ = cand[s]
             rows[r, pos] = new
-        fits = _fit_rows(plan, rows)
+        fits, sts = _eval_rows(plan, rows)
         fit_of = {s: float(fits[r]) for r, s in enumerate(keys)}
+        st_of = {s: int(sts[r]) for r, s in enumerate(keys)}
         # replay the reference's steps
         s = st0
         accepted = False
@@ -599,6 +600,8 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
             if s not in cand:
                 break
             pos, new, s2 = cand[s]
+            if st_of[s] >= N.ST_MISSING:  # the reference's fitness raises
+                _raise_status(st_of[s])
             cand_fit = fit_of[s]
             delta = cand_fit - cur_fit
             accept = delta <= 0
@@ -714,9 +717,14 @@ def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
             for r in range(j, len(muts)):
                 for pos, val in muts[r][0]:
                     rows[r - j, pos] = val
-            fits = _fit_rows(plan, rows) if V else np.zeros(len(rows))
+            if V:
+                fits, sts = _eval_rows(plan, rows)
+            else:
+                fits, sts = np.zeros(len(rows)), np.zeros(len(rows), np.uint8)
             acc = None
             for r in range(len(rows)):
+                if sts[r] >= N.ST_MISSING:  # the reference's fitness raises
+                    _raise_status(int(sts[r]))
                 if fits[r] <= cur_fit:
                     acc = r
                     break
