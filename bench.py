@@ -202,6 +202,8 @@ def time_to_solution(doc_name="ws_stack_10x20", budget=2000, seed=0):
     for algo in ("sa", "ea"):
         s, runs = run3(algo)
         assert s == aot[algo][0]
+        from paper_2308_00127_b200.heuristics import _last_chain_stats
+        stats = dict(_last_chain_stats)
         gpu_s = statistics.median(runs)
         t0 = time.perf_counter()
         fit, _ = (S.simulated_annealing(inst, 1, seed, budget) if algo == "sa"
@@ -212,6 +214,7 @@ def time_to_solution(doc_name="ws_stack_10x20", budget=2000, seed=0):
             "objective_ms": s.objective, "same_result": s.objective == fit,
             "gpu_runs_s": runs,
             "gpu_s_aot_body": statistics.median(aot[algo][1]),
+            "device_rounds": stats.get(f"{algo}_rounds"),
             "specialise_ms_not_timed": spec_ms,
             "gpu_path": ("one launch of K10 (speculative SA, PCG64 on the "
                          "device)" if algo == "sa" else

@@ -196,7 +196,7 @@ int hs_ea_run(const hs_plan *plan, uint8_t *d_parent, double cur_fit,
  * d_best [V] best-ever genome, d_rng = numpy PCG64 {state lo, state hi,
  * inc lo, inc hi}, d_buf = {has_uint32, uinteger}, d_f = {cur_fit,
  * best_fit, temp, -, -}, d_istate = {step, k (speculation window, start
- * 8), stop, status, pos, new}. Runs steps until `budget`; stop = 0 done,
+ * 8), stop, status, pos, new, rounds (accumulated)}. Runs steps until `budget`; stop = 0 done,
  * 2 a fitness evaluation raised (status = its code; GraphError), 3 the
  * Metropolis test at this step is within a few ulp of the device exp():
  * the caller decides it with the host exp (u = d_f[4], candidate fitness

@@ -123,8 +123,9 @@ struct SaParams {
     hs_u64 *rng;       // [4] PCG64 state lo, hi, increment lo, hi (in/out)
     hs_u32 *buf;       // [2] has_uint32, cached upper half (in/out)
     double *f;         // [5] cur, best, temp (in/out); stop 3: cand, u
-    int *istate;       // [6] step, k (in/out); stop (0 done, 2 raised, 3
-                       // host decides), raised status, stop 3: pos, new
+    int *istate;       // [7] step, k (in/out); stop (0 done, 2 raised, 3
+                       // host decides), raised status, stop 3: pos, new;
+                       // rounds (accumulated)
     int *spos;         // [window] speculative moves
     hs_u8 *snew;
     double *sfit;      // [window] speculative fitness, status
@@ -626,7 +627,7 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
     const hs_u32 nd1 = (hs_u32)(e.n_dev - 1);
     Pcg64 r;
     double cur = 0.0, bestf = 0.0, temp = 0.0;
-    int step = 0, stop = 0;
+    int step = 0, stop = 0, rounds = 0;
     if (l == 0) {
         r.slo = e.rng[0];
         r.shi = e.rng[1];
@@ -663,19 +664,22 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
             }
         }
         __syncthreads();
-        for (int i = 0; i < V; ++i) row[i] = genes[i];
         const bool valid = l < n;
-        if (valid) row[e.spos[l]] = e.snew[l];
-        double ms = 0.0;
-        int st = 0;
-        body.run(row, l, stp + l, valid, 0, ms, st);
-        if (valid) {
-            e.sfit[l] = ms;
-            e.sst[l] = (hs_u8)st;
+        if ((l & ~31) < n) {  // warp-uniform: warps past the window sit out
+            for (int i = 0; i < V; ++i) row[i] = genes[i];
+            if (valid) row[e.spos[l]] = e.snew[l];
+            double ms = 0.0;
+            int st = 0;
+            body.run(row, l, stp + l, valid, 0, ms, st);
+            if (valid) {
+                e.sfit[l] = ms;
+                e.sst[l] = (hs_u8)st;
+            }
         }
         __syncthreads();
         if (l == 0) {  // replay with the real generator
             bool acc = false;
+            ++rounds;
             for (int i = 0; i < n; ++i) {
                 const int pos = r.integers((hs_u32)V);
                 const int old = genes[pos];
@@ -735,6 +739,7 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
         e.istate[0] = step;
         e.istate[1] = s_k;
         e.istate[2] = stop;
+        e.istate[6] += rounds;
     }
 }
 
@@ -758,25 +763,33 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     hs_u8 *parent = e.parent;  // [V], global; written by one lane per round
     double cur = e.cur_fit;
     int acc = 0, rounds = 0, err_child = -1, err_st = 0;
+    // children per round: one warp after an acceptance, doubling while
+    // rounds reject (whole warps sit a round out: a lone warp's evaluation
+    // is the round's latency, and it is shortest without co-issuing warps)
+    int k = 32 < a.lanes ? 32 : a.lanes;
+    double ms = 0.0;
+    int st = 0;
     for (int j = 0; j < e.budget;) {
         if (l == 0) s_first = a.lanes;
         __syncthreads();  // parent / s_first of the previous round settled
-        for (int i = 0; i < a.V; ++i) row[i] = parent[i];
         const int c = j + l;
-        const bool valid = c < e.budget;
-        if (valid)
-            for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) row[e.mpos[q]] = e.mval[q];
-        double ms = 0.0;
-        int st = 0;
-        body.run(row, l, c, valid, 0, ms, st);
-        if (valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
+        const bool valid = l < k && c < e.budget;
+        if ((l & ~31) < k) {  // warp-uniform: the body may use warp-collective ops
+            for (int i = 0; i < a.V; ++i) row[i] = parent[i];
+            if (valid)
+                for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) row[e.mpos[q]] = e.mval[q];
+            body.run(row, l, c, valid, 0, ms, st);
+            if (valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
+        }
         __syncthreads();
         const int r = s_first;
         ++rounds;
         if (r == a.lanes) {
-            j += a.lanes;
+            j += k;
+            k = 2 * k < a.lanes ? 2 * k : a.lanes;
             continue;
         }
+        k = 32 < a.lanes ? 32 : a.lanes;
         if (l == r) {
             if (st >= ST_MISSING) {
                 s_fit = -1.0;

@@ -767,8 +767,9 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                   "hs_jit_trace(const EvalParams a) { jit_main<true, 0>(a, nullptr, nullptr); }\n",
                   T, T);
     s += buf;
-    if (jit_search_ok(p)) {
+    if (jit_search_ok(p) && o.sync == 0) {
         // single-CTA search drivers (SA K10, EA K9) over the specialised body
+        // (they leave idle warps out of a round: no CTA barriers in the body)
         std::snprintf(buf, sizeof buf,
                       "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
                       "hs_jit_sa(const EvalParams a, const SaParams e) "
@@ -992,9 +993,9 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     if (e == cudaSuccess)
         e = cudaKernelSetAttributeForDevice(
             m->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);
-    if (e == cudaSuccess && jit_search_ok(p)) {
-        e = cudaLibraryGetKernel(&m->kern_sa, m->lib, "hs_jit_sa");
-        if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kern_ea, m->lib, "hs_jit_ea");
+    if (e == cudaSuccess && jit_search_ok(p) &&
+        cudaLibraryGetKernel(&m->kern_sa, m->lib, "hs_jit_sa") == cudaSuccess) {
+        e = cudaLibraryGetKernel(&m->kern_ea, m->lib, "hs_jit_ea");
         if (e == cudaSuccess)
             e = cudaKernelSetAttributeForDevice(
                 m->kern_sa, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem), device);

@@ -469,6 +469,7 @@ def _fit_rows(plan: Plan, rows: np.ndarray) -> np.ndarray:
 
 
 _M64 = (1 << 64) - 1
+_last_chain_stats: dict = {}  # rounds of the last K9 / K10 run (reporting)
 
 
 def _sa_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
@@ -487,7 +488,7 @@ def _sa_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
                                 np.uint32).view(np.int32), device=dev)
     f = torch.tensor([cur_fit, best_fit, temp, 0.0, 0.0],
                      dtype=torch.float64, device=dev)
-    ist = torch.tensor([0, 8, 0, 0, 0, 0], dtype=torch.int32, device=dev)
+    ist = torch.tensor([0, 8, 0, 0, 0, 0, 0], dtype=torch.int32, device=dev)
     d_genes = torch.from_numpy(genes.copy()).to(dev)
     d_best = torch.from_numpy(genes.copy()).to(dev)
     while True:
@@ -511,8 +512,9 @@ def _sa_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
                 d_best.copy_(d_genes)
         f.copy_(torch.tensor([cur, bestf, tmp * alpha, 0.0, 0.0],
                              dtype=torch.float64))
-        ist.copy_(torch.tensor([int(iv[0]) + 1, 8, 0, 0, 0, 0],
+        ist.copy_(torch.tensor([int(iv[0]) + 1, 8, 0, 0, 0, 0, int(iv[6])],
                                dtype=torch.int32))
+    _last_chain_stats["sa_rounds"] = int(ist[6].item())
     w = rng.cpu().numpy().view(np.uint64)
     b = buf.cpu().numpy().view(np.uint32)
     bs["state"]["state"] = int(w[0]) | (int(w[1]) << 64)
@@ -659,6 +661,8 @@ def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
     plan.ea_run(d_parent, cur_fit, d_moff, d_mpos, d_mval, budget, d_fit,
                 d_info)
     info = d_info.cpu().numpy()
+    _last_chain_stats["ea_accepted"] = int(info[0])
+    _last_chain_stats["ea_rounds"] = int(info[1])
     if info[2] >= 0:
         _raise_status(int(info[3]))
     R.commit(gen, muts[-1][1])

@@ -271,7 +271,7 @@ class Plan:
                n_dev: int, budget: int, window: int, stream=None) -> None:
         """hs_sa_run (K10) on device tensors (all state in/out): genes /
         best uint8 [V], rng int64 [4] (PCG64 words), buf int32 [2], f f64
-        [5], istate int32 [6]."""
+        [5], istate int32 [7]."""
         N.check(self._lib.hs_sa_run(
             self.handle, _ptr(genes), _ptr(best), _ptr(rng), _ptr(buf),
             _ptr(f), _ptr(istate), float(alpha), int(n_dev), int(budget),
