@@ -619,10 +619,15 @@ struct Pcg64 {
 template <class Body>
 __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e, hs_u8 *smem,
                                          Body &body) {
-    __shared__ int s_k, s_step, s_go;
+    __shared__ int s_k, s_step, s_go, s_apos;
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
     hs_u8 *genes = e.genes;
+    // a lane's row stays the current genome between rounds: it undoes its
+    // own move and takes the round's accepted move (s_apos) instead of
+    // re-copying V bytes; a lane that sat a round out copies in full
+    int prev = -1;
+    bool synced = false;
     const int V = a.V, budget = e.budget;
     const hs_u32 nd1 = (hs_u32)(e.n_dev - 1);
     Pcg64 r;
@@ -642,6 +647,7 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
         s_k = e.istate[1];
         s_step = step;
         s_go = 1;
+        s_apos = -1;
     }
     __syncthreads();
     for (;;) {
@@ -666,8 +672,19 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
         __syncthreads();
         const bool valid = l < n;
         if ((l & ~31) < n) {  // warp-uniform: warps past the window sit out
-            for (int i = 0; i < V; ++i) row[i] = genes[i];
-            if (valid) row[e.spos[l]] = e.snew[l];
+            if (synced) {
+                if (prev >= 0) row[prev] = genes[prev];
+                const int ap = s_apos;
+                if (ap >= 0) row[ap] = genes[ap];
+            } else {
+                for (int i = 0; i < V; ++i) row[i] = genes[i];
+                synced = true;
+            }
+            prev = -1;
+            if (valid) {
+                prev = e.spos[l];
+                row[prev] = e.snew[l];
+            }
             double ms = 0.0;
             int st = 0;
             body.run(row, l, stp + l, valid, 0, ms, st);
@@ -675,11 +692,14 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
                 e.sfit[l] = ms;
                 e.sst[l] = (hs_u8)st;
             }
+        } else {
+            synced = false;
         }
         __syncthreads();
         if (l == 0) {  // replay with the real generator
             bool acc = false;
             ++rounds;
+            s_apos = -1;
             for (int i = 0; i < n; ++i) {
                 const int pos = r.integers((hs_u32)V);
                 const int old = genes[pos];
@@ -713,6 +733,7 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
                 ++step;
                 if (acc) {
                     genes[pos] = (hs_u8)nw;
+                    s_apos = pos;
                     cur = cand;
                     if (cand < bestf) {
                         bestf = cand;
@@ -769,32 +790,54 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     int k = 32 < a.lanes ? 32 : a.lanes;
     double ms = 0.0;
     int st = 0;
+    // a lane's row stays the parent between rounds: it undoes its own
+    // child's mutations and takes the accepted child's (cacc) instead of
+    // re-copying V bytes; a lane that sat a round out copies in full
+    int cprev = -1, cacc = -1;
+    bool synced = false;
     for (int j = 0; j < e.budget;) {
         if (l == 0) s_first = a.lanes;
         __syncthreads();  // parent / s_first of the previous round settled
         const int c = j + l;
         const bool valid = l < k && c < e.budget;
         if ((l & ~31) < k) {  // warp-uniform: the body may use warp-collective ops
-            for (int i = 0; i < a.V; ++i) row[i] = parent[i];
-            if (valid)
+            if (synced) {
+                if (cprev >= 0)
+                    for (int q = e.moff[cprev]; q < e.moff[cprev + 1]; ++q)
+                        row[e.mpos[q]] = parent[e.mpos[q]];
+                if (cacc >= 0)
+                    for (int q = e.moff[cacc]; q < e.moff[cacc + 1]; ++q)
+                        row[e.mpos[q]] = parent[e.mpos[q]];
+            } else {
+                for (int i = 0; i < a.V; ++i) row[i] = parent[i];
+                synced = true;
+            }
+            cprev = -1;
+            if (valid) {
+                cprev = c;
                 for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) row[e.mpos[q]] = e.mval[q];
+            }
             body.run(row, l, c, valid, 0, ms, st);
             if (valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
+        } else {
+            synced = false;
         }
         __syncthreads();
         const int r = s_first;
         ++rounds;
         if (r == a.lanes) {
+            cacc = -1;
             j += k;
             k = 2 * k < a.lanes ? 2 * k : a.lanes;
             continue;
         }
+        cacc = j + r;
         k = 32 < a.lanes ? 32 : a.lanes;
         if (l == r) {
             if (st >= ST_MISSING) {
                 s_fit = -1.0;
             } else {
-                for (int i = 0; i < a.V; ++i) parent[i] = row[i];
+                for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) parent[e.mpos[q]] = e.mval[q];
                 s_fit = ms;
             }
         }
