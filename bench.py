@@ -169,7 +169,8 @@ def c_port_rate(doc, cores):
 
 def time_to_solution(doc_name="ws_stack_10x20", budget=2000, seed=0):
     """Heuristic time-to-solution: the reference's SA and (1+1) EA
-    (heuristics.py:259-334) on the WS 10x20 stack, each run as one
+    (heuristics.py:259-334) on one instance (WS 10x20 stack, WS200, the
+    96-layer transformer on 30 devices), each run as one
     trajectory-exact device launch (this repo: K10 / K9) vs the CPU
     restatement that evaluates one candidate per step like the reference
     (oracle/hs_search.py). Both must end on the same genome."""
@@ -484,7 +485,9 @@ def main():
     tts = None
     if not args.no_tts:
         try:
-            tts = time_to_solution()
+            tts = {}
+            for name in ("ws_stack_10x20", "ws200", "tf96"):
+                tts.update(time_to_solution(name))
         except Exception as exc:  # reported, never fatal for the bench
             tts = {"error": repr(exc)}
 
