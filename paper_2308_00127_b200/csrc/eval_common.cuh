@@ -628,6 +628,9 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
     // re-copying V bytes; a lane that sat a round out copies in full
     int prev = -1;
     bool synced = false;
+    // the row's bytes past V stay 0 (the specialised body may read whole
+    // words of the row and rely on every byte being a valid gene)
+    for (int i = a.V; i < a.ld_s; ++i) row[i] = 0;
     const int V = a.V, budget = e.budget;
     const hs_u32 nd1 = (hs_u32)(e.n_dev - 1);
     Pcg64 r;
@@ -795,6 +798,9 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     // re-copying V bytes; a lane that sat a round out copies in full
     int cprev = -1, cacc = -1;
     bool synced = false;
+    // the row's bytes past V stay 0 (the specialised body may read whole
+    // words of the row and rely on every byte being a valid gene)
+    for (int i = a.V; i < a.ld_s; ++i) row[i] = 0;
     for (int j = 0; j < e.budget;) {
         if (l == 0) s_first = a.lanes;
         __syncthreads();  // parent / s_first of the previous round settled

@@ -1,0 +1,48 @@
+"""Per-run device time (CUDA events around the search launch) and wall time
+of SA / EA on one instance: separates GPU-side from host-side variance.
+
+    python tools/sa_timing.py [instance] [reps]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2308_00127_b200 as hs  # noqa: E402
+from paper_2308_00127_b200 import heuristics as H  # noqa: E402
+from conftest import instance_doc  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "ws_stack_10x20"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+g, hw, t = hs.load_instance(instance_doc(name))
+hs.specialize(g, hw, t, 1)
+orig = H.Plan.sa_run
+dev_ms = []
+
+
+def timed(self, *a, **k):
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    orig(self, *a, **k)
+    s1.record()
+    s1.synchronize()
+    dev_ms.append(s0.elapsed_time(s1))
+
+
+H.Plan.sa_run = timed
+for algo in ("sa", "ea"):
+    walls = []
+    for _ in range(reps):
+        w0 = time.perf_counter()
+        if algo == "sa":
+            hs.simulated_annealing(g, hw, t, 1, seed=0, budget=2000)
+        else:
+            hs.one_plus_one_ea(g, hw, t, 1, seed=0, budget=2000)
+        walls.append(round(1e3 * (time.perf_counter() - w0), 1))
+    print(name, algo, "wall ms", walls)
+print(name, "sa kernel ms", [round(x, 1) for x in dev_ms])
