@@ -125,3 +125,20 @@ def test_sa_host_exp_path(monkeypatch):
     monkeypatch.setenv("HS_SA_HOST_EXP", "1")
     b = hs.simulated_annealing(g, hw, t, 1, seed=2, budget=300)
     assert a == b
+
+
+def test_search_kernels_genes_in_registers(monkeypatch):
+    """The specialised body variant that reads whole words of the genome
+    row (HS_JIT_OPTS=genes=reg) gives the same SA / EA trajectories."""
+    from conftest import instance_doc
+    monkeypatch.setenv("HS_JIT_OPTS", "genes=reg")
+    g, hw, t = hs.load_instance(instance_doc("ws30"))  # fresh plan objects
+    hs.specialize(g, hw, t, 1)
+    for seed in (1, 5):
+        assert hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=500) == \
+            hs.simulated_annealing(g, hw, t, 1, seed=seed, budget=500,
+                                   device_chain=False)
+        assert hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=500,
+                                  biased=False) == \
+            hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=500,
+                               biased=False, device_chain=False)
