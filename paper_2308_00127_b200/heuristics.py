@@ -17,6 +17,8 @@ that consume it -- the drop-in for ``hetsched.heuristics``
 """
 from __future__ import annotations
 
+import functools
+import gc
 import math
 import threading
 from dataclasses import dataclass
@@ -468,6 +470,23 @@ def _fit_rows(plan: Plan, rows: np.ndarray) -> np.ndarray:
     return ms
 
 
+def _gc_paused(fn):
+    """Run a search loop with the cyclic garbage collector paused (and
+    restored after): a full collection over torch's object graph costs
+    50 ms - 1.8 s of wall time in the middle of a 10-50 ms run (measured,
+    profiles/README.md r1o); cycles created meanwhile are collected later."""
+    @functools.wraps(fn)
+    def run(*a, **k):
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            return fn(*a, **k)
+        finally:
+            if was:
+                gc.enable()
+    return run
+
+
 _M64 = (1 << 64) - 1
 _last_chain_stats: dict = {}  # rounds of the last K9 / K10 run (reporting)
 
@@ -523,6 +542,7 @@ def _sa_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
     return d_best.cpu().numpy(), float(f[1].item())
 
 
+@_gc_paused
 def simulated_annealing(g, hw, table, L: int, seed: int = 0,
                         budget: int = 2000, t0_fraction: float = 0.1,
                         alpha: float = 0.995, window: int = 64,
@@ -669,6 +689,7 @@ def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
     return d_parent.cpu().numpy(), float(d_fit.cpu()[0])
 
 
+@_gc_paused
 def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
                     biased: bool = True, window: int = 256,
                     device_chain: bool = True) -> Schedule:

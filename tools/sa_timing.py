@@ -35,6 +35,9 @@ def timed(self, *a, **k):
 
 
 H.Plan.sa_run = timed
+if os.environ.get("NOGC"):
+    import gc
+    gc.disable()
 for algo in ("sa", "ea"):
     walls = []
     for _ in range(reps):
