@@ -414,6 +414,8 @@ int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *
     e.mpos = mpos;
     e.mval = mval;
     e.budget = budget;
+    const char *lv = getenv("HS_EA_LEVELS");
+    e.two_level = lv ? atoi(lv) >= 2 : 1;
     e.out_fit = out_fit;
     e.info = info;
     CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));

@@ -112,6 +112,7 @@ struct EaParams {
     const int *mpos;      // mutated genome positions
     const hs_u8 *mval;    // new genes
     int budget;
+    int two_level;        // evaluate children of child j speculatively
     double *out_fit;      // [1] final fitness
     int *info;            // [4] accepted, rounds, raising child (-1), status
 };
@@ -780,11 +781,11 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
 template <class Body>
 __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e, hs_u8 *smem,
                                          Body &body) {
-    __shared__ int s_first;
-    __shared__ double s_fit;
+    __shared__ int s_first, s_first2;
+    __shared__ double s_fit, s_fit2;
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
-    hs_u8 *parent = e.parent;  // [V], global; written by one lane per round
+    hs_u8 *parent = e.parent;  // [V], global; written by one lane per acceptance
     double cur = e.cur_fit;
     int acc = 0, rounds = 0, err_child = -1, err_st = 0;
     // children per round: one warp after an acceptance, doubling while
@@ -793,52 +794,65 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     int k = 32 < a.lanes ? 32 : a.lanes;
     double ms = 0.0;
     int st = 0;
-    // a lane's row stays the parent between rounds: it undoes its own
-    // child's mutations and takes the accepted child's (cacc) instead of
-    // re-copying V bytes; a lane that sat a round out copies in full
-    int cprev = -1, cacc = -1;
+    // a lane's row stays the parent between rounds: it undoes the
+    // mutations it applied (its child's, and child j's on the second level)
+    // and takes the accepted children's (cacc, cacc2) instead of re-copying
+    // V bytes; a lane that sat a round out copies in full
+    int bprev = -1, cprev = -1, cacc = -1, cacc2 = -1;
     bool synced = false;
     // the row's bytes past V stay 0 (the specialised body may read whole
     // words of the row and rely on every byte being a valid gene)
     for (int i = a.V; i < a.ld_s; ++i) row[i] = 0;
     for (int j = 0; j < e.budget;) {
-        if (l == 0) s_first = a.lanes;
+        if (l == 0) {
+            s_first = a.lanes;
+            s_first2 = 32;
+        }
         __syncthreads();  // parent / s_first of the previous round settled
-        const int c = j + l;
-        const bool valid = l < k && c < e.budget;
-        if ((l & ~31) < k) {  // warp-uniform: the body may use warp-collective ops
+        // second level: one more warp evaluates children j+1.. on top of
+        // child j, for the case that child j is accepted (the commonest
+        // first acceptance) -- then one round makes two acceptances
+        const bool lvl2 = e.two_level && k + 32 <= a.lanes;
+        const int w0 = l & ~31;
+        const int c = w0 < k ? j + l : j + 1 + (l - k);
+        const bool valid = c < e.budget && (w0 < k ? l < k : lvl2 && w0 == k);
+        if (w0 < k || (lvl2 && w0 == k)) {  // warp-uniform (warp-collective body ops)
+            const bool is2 = w0 >= k;
             if (synced) {
-                if (cprev >= 0)
-                    for (int q = e.moff[cprev]; q < e.moff[cprev + 1]; ++q)
-                        row[e.mpos[q]] = parent[e.mpos[q]];
-                if (cacc >= 0)
-                    for (int q = e.moff[cacc]; q < e.moff[cacc + 1]; ++q)
-                        row[e.mpos[q]] = parent[e.mpos[q]];
+                const int undo[4] = {bprev, cprev, cacc, cacc2};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (undo[u] >= 0)
+                        for (int q = e.moff[undo[u]]; q < e.moff[undo[u] + 1]; ++q)
+                            row[e.mpos[q]] = parent[e.mpos[q]];
             } else {
                 for (int i = 0; i < a.V; ++i) row[i] = parent[i];
                 synced = true;
             }
-            cprev = -1;
+            bprev = cprev = -1;
+            if (is2) {  // second level: on top of child j
+                bprev = j;
+                for (int q = e.moff[j]; q < e.moff[j + 1]; ++q) row[e.mpos[q]] = e.mval[q];
+            }
             if (valid) {
                 cprev = c;
                 for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) row[e.mpos[q]] = e.mval[q];
             }
             body.run(row, l, c, valid, 0, ms, st);
-            if (valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
+            if (!is2 && valid && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first, l);
         } else {
             synced = false;
         }
         __syncthreads();
         const int r = s_first;
         ++rounds;
+        cacc = cacc2 = -1;
         if (r == a.lanes) {
-            cacc = -1;
             j += k;
             k = 2 * k < a.lanes ? 2 * k : a.lanes;
             continue;
         }
         cacc = j + r;
-        k = 32 < a.lanes ? 32 : a.lanes;
         if (l == r) {
             if (st >= ST_MISSING) {
                 s_fit = -1.0;
@@ -855,7 +869,39 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
         }
         cur = s_fit;
         ++acc;
-        j += r + 1;
+        const int k1 = k;
+        k = 32 < a.lanes ? 32 : a.lanes;
+        if (r != 0 || !lvl2) {
+            j += r + 1;
+            continue;
+        }
+        // child j was accepted: the second level's children are children
+        // j+1.. of the new parent
+        if (valid && w0 == k1 && (st >= ST_MISSING || ms <= cur)) atomicMin(&s_first2, l - k1);
+        __syncthreads();
+        const int r2 = s_first2;
+        if (r2 == 32) {
+            j += 1 + 32;
+            continue;
+        }
+        if (w0 == k1 && l - k1 == r2) {
+            if (st >= ST_MISSING) {
+                s_fit2 = -1.0;
+            } else {
+                for (int q = e.moff[c]; q < e.moff[c + 1]; ++q) parent[e.mpos[q]] = e.mval[q];
+                s_fit2 = ms;
+            }
+        }
+        __syncthreads();
+        if (s_fit2 < 0.0) {
+            err_child = j + 1 + r2;
+            if (w0 == k1 && l - k1 == r2) err_st = st;
+            break;
+        }
+        cur = s_fit2;
+        ++acc;
+        cacc2 = j + 1 + r2;
+        j += r2 + 2;
     }
     if (err_st) e.info[3] = err_st;  // the raising lane only
     if (l == 0) {
