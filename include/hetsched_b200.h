@@ -191,6 +191,17 @@ int hs_ea_run(const hs_plan *plan, uint8_t *d_parent, double cur_fit,
               const int32_t *d_moff, const int32_t *d_mpos, const uint8_t *d_mval,
               int32_t budget, double *d_fit, int32_t *d_info, void *stream);
 
+/* The same accept chain in chained chunks, so the caller can draw the next
+ * chunk's mutations while this one runs: children first_child ..
+ * first_child + n_children - 1 with CSR lists relative to the chunk; the
+ * current fitness is read from and written back to d_fit[0]; d_info
+ * accumulates (the caller sets it to {0, 0, -1, 0} once) and a chunk does
+ * nothing when an earlier one raised (d_info[2] >= 0, absolute child). */
+int hs_ea_run_chunk(const hs_plan *plan, uint8_t *d_parent, double *d_fit,
+                    const int32_t *d_moff, const int32_t *d_mpos, const uint8_t *d_mval,
+                    int32_t n_children, int32_t first_child, int32_t *d_info,
+                    void *stream);
+
 /* Simulated annealing (heuristics.py:259-299) in one launch, resumable.
  * All state lives in device buffers (in/out): d_genes [V] current genome,
  * d_best [V] best-ever genome, d_rng = numpy PCG64 {state lo, state hi,

@@ -397,7 +397,8 @@ int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalPar
 
 int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *moff,
            const int32_t *mpos, const uint8_t *mval, int32_t budget, double *out_fit,
-           int32_t *info, cudaStream_t stream) {
+           int32_t *info, cudaStream_t stream, const double *cur_in = nullptr,
+           int32_t first_child = -1) {
     if (budget < 0 || !parent || !out_fit || !info || (budget > 0 && !moff))
         return set_err(HS_EINVAL, "bad EA arguments");
     const hs::DevState *ds = nullptr;
@@ -418,7 +419,10 @@ int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *
     e.two_level = lv ? atoi(lv) >= 2 : 1;
     e.out_fit = out_fit;
     e.info = info;
-    CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));
+    e.cur_in = cur_in;
+    e.first_child = first_child;
+    e.accumulate = first_child >= 0;
+    if (!e.accumulate) CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));
     rc = jm ? hs::jit_launch_search(*jm, 2, a, &e, stream, &err)
             : hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err);
     if (rc) return set_err(rc, err);
@@ -837,6 +841,15 @@ int hs_ea_run(const hs_plan *plan, uint8_t *d_parent, double cur_fit,
               int32_t budget, double *d_fit, int32_t *d_info, void *stream) {
     return run_ea(plan, d_parent, cur_fit, d_moff, d_mpos, d_mval, budget, d_fit, d_info,
                   static_cast<cudaStream_t>(stream));
+}
+
+int hs_ea_run_chunk(const hs_plan *plan, uint8_t *d_parent, double *d_fit,
+                    const int32_t *d_moff, const int32_t *d_mpos, const uint8_t *d_mval,
+                    int32_t n_children, int32_t first_child, int32_t *d_info,
+                    void *stream) {
+    if (first_child < 0 || !d_fit) return set_err(HS_EINVAL, "bad EA chunk arguments");
+    return run_ea(plan, d_parent, 0.0, d_moff, d_mpos, d_mval, n_children, d_fit, d_info,
+                  static_cast<cudaStream_t>(stream), d_fit, first_child);
 }
 
 int hs_sa_run(const hs_plan *plan, uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng,

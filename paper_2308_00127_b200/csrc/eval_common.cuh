@@ -113,6 +113,10 @@ struct EaParams {
     const hs_u8 *mval;    // new genes
     int budget;
     int two_level;        // evaluate children of child j speculatively
+    // chained chunks (hs_ea_run_chunk): fitness read from cur_in, counters
+    // accumulated into info, nothing done when an earlier chunk raised
+    const double *cur_in;
+    int first_child, accumulate;
     double *out_fit;      // [1] final fitness
     int *info;            // [4] accepted, rounds, raising child (-1), status
 };
@@ -786,7 +790,8 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
     hs_u8 *parent = e.parent;  // [V], global; written by one lane per acceptance
-    double cur = e.cur_fit;
+    if (e.accumulate && e.info[2] >= 0) return;  // an earlier chunk raised
+    double cur = e.cur_in ? *e.cur_in : e.cur_fit;
     int acc = 0, rounds = 0, err_child = -1, err_st = 0;
     // children per round: one warp after an acceptance, doubling while
     // rounds reject (whole warps sit a round out: a lone warp's evaluation
@@ -906,9 +911,15 @@ __device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e,
     if (err_st) e.info[3] = err_st;  // the raising lane only
     if (l == 0) {
         e.out_fit[0] = cur;
-        e.info[0] = acc;
-        e.info[1] = rounds;
-        e.info[2] = err_child;
+        if (e.accumulate) {
+            e.info[0] += acc;
+            e.info[1] += rounds;
+            if (err_child >= 0) e.info[2] = e.first_child + err_child;
+        } else {
+            e.info[0] = acc;
+            e.info[1] = rounds;
+            e.info[2] = err_child;
+        }
     }
 }
 

@@ -652,40 +652,63 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     return out
 
 
-def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
-                     budget: int, V: int, n_dev: int, p: float):
-    """Every child's mutations drawn up front, then the whole accept chain
-    in one kernel launch (hs_ea_run, K9). Returns (genes, fitness)."""
+def _ea_draw_chunk(gen, steps: int, V: int, n_dev: int, p: float):
+    """Mutation lists of the next `steps` EA children as CSR arrays in
+    pinned host memory; moves `gen` past them."""
     import torch
-    need = budget * (V + 2) + 64
+    need = steps * (V + 2) + 64
     while True:
         S, words, st = R.peek_words(gen, need)
         try:
-            muts = R.ea_mutations(S, words, st, budget, V, n_dev, p)
+            muts = R.ea_mutations(S, words, st, steps, V, n_dev, p)
             break
         except IndexError:
             need *= 2
-    counts = np.fromiter((len(m[0]) for m in muts), np.int32, budget)
-    moff = np.zeros(budget + 1, np.int32)
-    np.cumsum(counts, out=moff[1:])
+    R.commit(gen, muts[-1][1])
+    counts = np.fromiter((len(m[0]) for m in muts), np.int32, steps)
     flat = [pv for m in muts for pv in m[0]]
-    mpos = np.fromiter((pv[0] for pv in flat), np.int32, len(flat))
-    mval = np.fromiter((pv[1] for pv in flat), np.uint8, len(flat))
+    moff = torch.empty(steps + 1, dtype=torch.int32, pin_memory=True)
+    mn = moff.numpy()
+    mn[0] = 0
+    np.cumsum(counts, out=mn[1:])
+    mpos = torch.empty(max(len(flat), 1), dtype=torch.int32, pin_memory=True)
+    mval = torch.empty(max(len(flat), 1), dtype=torch.uint8, pin_memory=True)
+    if flat:
+        mpos.numpy()[:len(flat)] = np.fromiter((pv[0] for pv in flat), np.int32,
+                                               len(flat))
+        mval.numpy()[:len(flat)] = np.fromiter((pv[1] for pv in flat), np.uint8,
+                                               len(flat))
+    return moff, mpos[:len(flat)], mval[:len(flat)]
+
+
+def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
+                     budget: int, V: int, n_dev: int, p: float,
+                     chunks: int = 4):
+    """The accept chain on the device (K9) in `chunks` chained launches
+    (hs_ea_run_chunk): the host draws chunk c+1's mutations while chunk c
+    runs. Returns (genes, fitness)."""
+    import torch
     dev = torch.device("cuda")
+    stream = torch.cuda.current_stream()
     d_parent = torch.from_numpy(genes.copy()).to(dev)
-    d_moff = torch.from_numpy(moff).to(dev)
-    d_mpos = torch.from_numpy(mpos).to(dev)
-    d_mval = torch.from_numpy(mval).to(dev)
-    d_fit = torch.empty(1, dtype=torch.float64, device=dev)
-    d_info = torch.empty(4, dtype=torch.int32, device=dev)
-    plan.ea_run(d_parent, cur_fit, d_moff, d_mpos, d_mval, budget, d_fit,
-                d_info)
+    d_fit = torch.tensor([cur_fit], dtype=torch.float64, device=dev)
+    d_info = torch.tensor([0, 0, -1, 0], dtype=torch.int32, device=dev)
+    size = -(-budget // max(1, chunks))
+    keep = []  # device copies must outlive their (asynchronous) launches
+    first = 0
+    while first < budget:
+        n = min(size, budget - first)
+        moff, mpos, mval = _ea_draw_chunk(gen, n, V, n_dev, p)
+        d = [x.to(dev, non_blocking=True) for x in (moff, mpos, mval)]
+        keep.append((moff, mpos, mval, d))
+        plan.ea_run_chunk(d_parent, d_fit, d[0], d[1], d[2], n, first, d_info,
+                          stream=stream)
+        first += n
     info = d_info.cpu().numpy()
     _last_chain_stats["ea_accepted"] = int(info[0])
     _last_chain_stats["ea_rounds"] = int(info[1])
     if info[2] >= 0:
         _raise_status(int(info[3]))
-    R.commit(gen, muts[-1][1])
     return d_parent.cpu().numpy(), float(d_fit.cpu()[0])
 
 

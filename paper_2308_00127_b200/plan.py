@@ -267,6 +267,16 @@ class Plan:
             _ptr(mval) if mval.numel() else None, int(budget), _ptr(fit),
             _ptr(info), self._stream(stream)), "hs_ea_run")
 
+    def ea_run_chunk(self, parent, fit, moff, mpos, mval, n_children: int,
+                     first_child: int, info, stream=None) -> None:
+        """hs_ea_run_chunk (K9 in chained chunks) on device tensors."""
+        N.check(self._lib.hs_ea_run_chunk(
+            self.handle, _ptr(parent), _ptr(fit), _ptr(moff),
+            _ptr(mpos) if mpos.numel() else None,
+            _ptr(mval) if mval.numel() else None, int(n_children),
+            int(first_child), _ptr(info), self._stream(stream)),
+            "hs_ea_run_chunk")
+
     def sa_run(self, genes, best, rng, buf, f, istate, alpha: float,
                n_dev: int, budget: int, window: int, stream=None) -> None:
         """hs_sa_run (K10) on device tensors (all state in/out): genes /
