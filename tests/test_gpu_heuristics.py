@@ -142,3 +142,30 @@ def test_search_kernels_genes_in_registers(monkeypatch):
                                   biased=False) == \
             hs.one_plus_one_ea(g, hw, t, 1, seed=seed, budget=500,
                                biased=False, device_chain=False)
+
+
+def test_ea_single_launch_equals_chunks():
+    """hs_ea_run (whole chain, one launch) and hs_ea_run_chunk (chained
+    chunks, the default path) end on the same genome and fitness."""
+    import numpy as np
+    from conftest import instance_doc
+    from paper_2308_00127_b200 import heuristics as H
+    g, hw, t = hs.load_instance(instance_doc("ws_stack_10x20"))
+    plan = H.get_plan(g, hw, t, 1)
+    V, K = plan.V, plan.K
+    genes0 = np.random.default_rng(9).integers(K, size=V, dtype=np.uint8)
+    f0 = float(hs.fitness_batch(genes0[None, :], g, hw, t, 1)[0])
+    budget = 900
+    moff, mpos, mval = H._ea_draw_chunk(np.random.default_rng(3), budget, V,
+                                        K, 1.0 / V)
+    parent = torch.from_numpy(genes0.copy()).cuda()
+    fit = torch.empty(1, dtype=torch.float64, device="cuda")
+    info = torch.empty(4, dtype=torch.int32, device="cuda")
+    plan.ea_run(parent, f0, moff.cuda(), mpos.cuda(), mval.cuda(), budget,
+                fit, info)
+    for chunks in (1, 3, 7):
+        g2, f2 = H._ea_device_chain(plan, np.random.default_rng(3), genes0,
+                                    f0, budget, V, K, 1.0 / V, chunks=chunks)
+        assert np.array_equal(g2, parent.cpu().numpy()), chunks
+        assert f2 == float(fit.cpu()[0]), chunks
+    assert int(info.cpu()[2]) == -1
