@@ -641,6 +641,7 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
     Pcg64 r;
     double cur = 0.0, bestf = 0.0, temp = 0.0;
     int step = 0, stop = 0, rounds = 0;
+    if (e.istate[2] != 0) return;  // a chained earlier launch stopped
     if (l == 0) {
         r.slo = e.rng[0];
         r.shi = e.rng[1];

@@ -35,6 +35,22 @@ def timed(self, *a, **k):
 
 
 H.Plan.sa_run = timed
+parts = {"greedy": [], "chain": [], "decode": []}
+
+
+def _timed_part(name, fn):
+    def run(*a, **k):
+        w0 = time.perf_counter()
+        try:
+            return fn(*a, **k)
+        finally:
+            parts[name].append(round(1e3 * (time.perf_counter() - w0), 1))
+    return run
+
+
+H.greedy = _timed_part("greedy", H.greedy)
+H._sa_device_chain = _timed_part("chain", H._sa_device_chain)
+H.decode = _timed_part("decode", H.decode)
 if os.environ.get("NOGC"):
     import gc
     gc.disable()
@@ -49,3 +65,5 @@ for algo in ("sa", "ea"):
         walls.append(round(1e3 * (time.perf_counter() - w0), 1))
     print(name, algo, "wall ms", walls)
 print(name, "sa kernel ms", [round(x, 1) for x in dev_ms])
+for k, v in parts.items():
+    print(name, "part", k, v[:reps])
