@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from .core import GraphError, Schedule, ScheduledBatch
-from .heuristics import INF, _raise_status
+from .heuristics import INF, _batch_genes, _raise_status
 from .plan import get_plan
 
 
@@ -39,6 +39,7 @@ def fitness_batched(genes, g, hw, table, L: int, *,
     """Makespans of extended genomes uint8 [n, >=V] (numpy -> host path,
     CUDA tensor -> device path)."""
     plan = _plan(g, hw, table, L, splits)
+    genes = _batch_genes(genes, plan.V)
     if hasattr(genes, "data_ptr"):
         import torch
         n = genes.shape[0]
@@ -50,7 +51,6 @@ def fitness_batched(genes, g, hw, table, L: int, *,
         if n and int(st.max().item()) >= N.ST_MISSING:
             _raise_status(int(st.max().item()))
         return ms
-    genes = np.ascontiguousarray(genes, np.uint8)
     ms = np.empty(len(genes), np.float64)
     st = np.empty(len(genes), np.uint8)
     if len(genes):

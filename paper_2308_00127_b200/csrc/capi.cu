@@ -764,7 +764,11 @@ static int eval_host_impl(const hs_plan *plan, const uint8_t *h_genes, int64_t n
             uint8_t *dsx = reinterpret_cast<uint8_t *>(dm + chunk);
             const int64_t lo = c * chunk, rows = std::min(chunk, n - lo);
             if (rows > 0) {
-                e = cudaMemcpyAsync(dg, h_genes + lo * ld, size_t(rows * ld),
+                // the last row ends at its last gene byte: a row-strided view
+                // owns nothing past it
+                const int64_t row_bytes = packed ? ld : plan->p.V;
+                e = cudaMemcpyAsync(dg, h_genes + lo * ld,
+                                    size_t((rows - 1) * ld + row_bytes),
                                     cudaMemcpyHostToDevice, s);
                 if (e != cudaSuccess) {
                     rc = cuda_err(e, "H2D genes");

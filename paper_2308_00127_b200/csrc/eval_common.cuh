@@ -653,7 +653,9 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
         bestf = e.f[1];
         temp = e.f[2];
         step = e.istate[0];
-        s_k = e.istate[1];
+        // the first round's window comes from the caller: at most the
+        // scratch arrays' length (e.window <= lanes)
+        s_k = e.istate[1] < 1 ? 1 : (e.istate[1] < e.window ? e.istate[1] : e.window);
         s_step = step;
         s_go = 1;
         s_apos = -1;
@@ -729,7 +731,11 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
                 if (!acc && fin) {
                     const double u = r.random();
                     const double ex = exp(-delta / temp);
-                    if (e.host_exp || u == 0.0 || fabs(u - ex) <= ex * 0x1p-48) {
+                    // temp == 0 (cooled to underflow): the reference's
+                    // -delta / temp raises ZeroDivisionError -- the host's
+                    // Python division decides, as it does for a close call
+                    if (e.host_exp || temp == 0.0 || u == 0.0 ||
+                        fabs(u - ex) <= ex * 0x1p-48) {
                         stop = 3;  // too close to call against CPython's exp
                         e.istate[4] = pos;
                         e.istate[5] = nw;

@@ -116,6 +116,35 @@ def _eval_rows(plan: Plan, rows: np.ndarray, trace: bool = False):
     return out
 
 
+def _batch_genes(genes, V: int):
+    """The one input check of every batched entry point (fitness_batch,
+    argmin_batch, fitness_batch_packed, fitness_batched). A CUDA tensor
+    must be uint8 [n, >=V] with unit column stride and rows that do not
+    overlap (stride(0) >= shape[1]); values >= K are reported by the kernel
+    (status 5, GraphError). A host array is brought to uint8 with every
+    value outside [0, 255] mapped to 255, so it stays out of range (status
+    5) instead of wrapping into a valid gene."""
+    if hasattr(genes, "data_ptr"):  # torch tensor on the GPU
+        import torch
+        if genes.dtype != torch.uint8 or genes.dim() != 2 \
+                or genes.shape[1] < V:
+            raise GraphError("genes must be a uint8 [n, >=V] tensor")
+        if genes.numel() and (genes.stride(1) != 1 or (
+                genes.shape[0] > 1 and genes.stride(0) < genes.shape[1])):
+            raise GraphError("genes must be row-major with non-overlapping "
+                             "rows (stride(1) == 1, stride(0) >= shape[1])")
+        return genes
+    genes = np.asarray(genes)
+    if genes.ndim != 2 or genes.shape[1] < V:
+        raise GraphError("genes must be a [n, >=V] array")
+    if genes.dtype != np.uint8:
+        if genes.dtype.kind not in "iub":
+            raise GraphError("genes must be integers")
+        genes = np.where((genes < 0) | (genes > 255), 255,
+                         genes).astype(np.uint8)
+    return genes
+
+
 def _check_genes(genes: Sequence[int], K: int) -> None:
     # heuristics.py:133-134: validated before any placement
     if any(not 0 <= int(k) < K for k in genes):
@@ -181,12 +210,9 @@ def fitness_batch(genes, g, hw, table, L: int, *,
     case (makespan, status) is returned.
     """
     plan = get_plan(g, hw, table, L, order)
+    genes = _batch_genes(genes, plan.V)
     if hasattr(genes, "data_ptr"):  # torch tensor on the GPU
         import torch
-        if genes.dtype != torch.uint8 or genes.dim() != 2 \
-                or genes.shape[1] < plan.V or (genes.numel() and
-                                               genes.stride(1) != 1):
-            raise GraphError("genes must be a uint8 [n, >=V] row-major tensor")
         n = genes.shape[0]
         plan.maybe_specialize(n)
         ms = torch.empty(n, dtype=torch.float64, device=genes.device)
@@ -199,16 +225,6 @@ def fitness_batch(genes, g, hw, table, L: int, *,
             bad = int(torch.nonzero(st >= N.ST_MISSING)[0].item())
             _raise_status(int(st[bad].item()))
         return ms
-    genes = np.asarray(genes)
-    if genes.ndim != 2 or genes.shape[1] < plan.V:
-        raise GraphError("genes must be a [n, >=V] array")
-    if genes.dtype != np.uint8:
-        out_of_range = (genes < 0) | (genes >= plan.K)
-        if out_of_range.any() and not return_status:
-            raise GraphError("gene value out of device range")
-        # anything outside [0, 255] becomes 255 (still out of range: status 5)
-        genes = np.where((genes < 0) | (genes > 255), 255,
-                         genes).astype(np.uint8)
     n = genes.shape[0]
     plan.maybe_specialize(n)
     ms = np.empty(n, np.float64)
@@ -259,6 +275,9 @@ def fitness_batch_packed(packed, g, hw, table, L: int, *,
     if radix not in (3, 4):
         raise ValueError("radix must be 3 or 4")
     plan = get_plan(g, hw, table, L)
+    # bytes a packed row needs (2-bit: ceil(V/4); base 3: ceil(V/5))
+    packed = _batch_genes(packed, (plan.V + 3) // 4 if radix == 4
+                          else plan.packed3_ld())
     n = int(packed.shape[0])
     plan.maybe_specialize(n)
     if hasattr(packed, "data_ptr"):
@@ -305,16 +324,26 @@ def argmin_batch(genes, g, hw, table, L: int, *,
     """(makespan, index) of the first best genome (numpy.argmin semantics,
     +inf allowed) computed by the fused on-device reduction."""
     plan = get_plan(g, hw, table, L, order)
-    plan.maybe_specialize(int(genes.shape[0]))
+    genes = _batch_genes(genes, plan.V)
+    n = int(genes.shape[0])
+    plan.maybe_specialize(n)
     if hasattr(genes, "data_ptr"):
         import torch
         best = torch.empty(2, dtype=torch.int64, device=genes.device)
-        plan.eval(genes, None, None, best, index_base)
+        st = torch.empty(n, dtype=torch.uint8, device=genes.device)
+        plan.eval(genes, None, st, best, index_base)
+        # the reference's fitness raises on these (GraphError), it does not
+        # score them +inf
+        if n and int(st.max().item()) >= N.ST_MISSING:
+            bad = int(torch.nonzero(st >= N.ST_MISSING)[0].item())
+            _raise_status(int(st[bad].item()))
         b = best.cpu()
         return float(b[:1].view(torch.float64).item()), int(b[1].item())
-    genes = np.ascontiguousarray(genes, np.uint8)
     b = N.Best()
-    plan.eval_host(genes, None, None, b, index_base)
+    st = np.empty(n, np.uint8)
+    plan.eval_host(genes, None, st, b, index_base)
+    if n and st.max() >= N.ST_MISSING:
+        _raise_status(int(st[np.argmax(st >= N.ST_MISSING)]))
     return float(b.cost), int(b.index)
 
 

@@ -2,9 +2,14 @@
 native ``hs_plan`` handle, plus the device-side entry points that use it.
 
 A plan is compiled once per instance by the native plan compiler
-(csrc/plan.cpp) and cached on object identity: the reference's graph,
-hardware and latency objects are immutable after construction
-(core.py:38 of the reference), so identity is a sound key.
+(csrc/plan.cpp) and cached on object identity plus a cheap shape
+fingerprint (entry / link / device counts). The reference declares every
+type immutable after construction (SPEC.md, "Concurrency Model"; core.py:38),
+but ``LatencyTable.entries`` and
+``HardwareSystem.bandwidth`` are plain dicts: adding or removing entries
+after a first evaluation is detected (new plan), editing a value in place
+is not -- build a new table / hardware object instead (a full content hash
+would cost more than a small evaluation on every call).
 """
 from __future__ import annotations
 
@@ -208,7 +213,11 @@ class Plan:
              index_base: int = 0, stream=None) -> None:
         """hs_eval on device tensors: genes uint8 [n, ld] (ld >= V)."""
         n = int(genes.shape[0])
-        ld = max(int(genes.stride(0)), self.V) if genes.numel() else self.V
+        ld = int(genes.stride(0)) if n > 1 else max(int(genes.shape[1]),
+                                                     self.V)
+        if n > 1 and ld < self.V:
+            raise GraphError(f"genome rows overlap: stride(0) = {ld} < V = "
+                             f"{self.V}")
         N.check(self._lib.hs_eval(
             self.handle, genes.data_ptr() if genes.numel() else None, n, ld,
             _ptr(makespan), _ptr(status), _ptr(best), int(index_base),
@@ -218,10 +227,13 @@ class Plan:
                   best: Optional[N.Best] = None, index_base: int = 0,
                   stream=None) -> None:
         """hs_eval_host: numpy uint8 [n, ld] host genes, results to host."""
-        genes = np.ascontiguousarray(genes, dtype=np.uint8) \
-            if genes.strides[-1] != 1 else genes
         n = genes.shape[0]
-        # a length-1 leading axis may carry stride 0 (x[None, :])
+        # rows must be unit-stride and non-overlapping (a view such as
+        # genes[::-1] or a broadcast is copied); a length-1 leading axis may
+        # carry stride 0 (x[None, :])
+        if genes.dtype != np.uint8 or genes.strides[-1] != 1 or (
+                n > 1 and genes.strides[0] < genes.shape[1]):
+            genes = np.ascontiguousarray(genes, dtype=np.uint8)
         ld = genes.strides[0] if n > 1 else max(genes.shape[1], self.V)
         N.check(self._lib.hs_eval_host(
             self.handle, genes.ctypes.data if n else None, n, ld,
@@ -247,6 +259,7 @@ class Plan:
     def eval_host_packed(self, packed: np.ndarray, makespan=None, status=None,
                          best: Optional[N.Best] = None, index_base: int = 0,
                          stream=None) -> None:
+        packed = np.ascontiguousarray(packed, dtype=np.uint8)
         n = packed.shape[0]
         ld = packed.strides[0] if n > 1 else self.packed_ld()
         N.check(self._lib.hs_eval_host_packed(
@@ -304,6 +317,7 @@ class Plan:
     def eval_host_packed3(self, packed: np.ndarray, makespan=None,
                           status=None, best: Optional[N.Best] = None,
                           index_base: int = 0, stream=None) -> None:
+        packed = np.ascontiguousarray(packed, dtype=np.uint8)
         n = packed.shape[0]
         ld = packed.strides[0] if n > 1 else self.packed3_ld()
         N.check(self._lib.hs_eval_host_packed3(
@@ -377,6 +391,12 @@ def _ref(o):
         return lambda o=o: o  # not weak-referenceable: hold it
 
 
+def _fingerprint(g, hw, table) -> tuple:
+    return (len(g.tasks), len(getattr(g, "edges", ())),
+            len(hw.devices), len(getattr(hw, "bandwidth", ())),
+            len(getattr(table, "entries", ())))
+
+
 def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None,
              batched: Optional[tuple] = None) -> Plan:
     """Cached plan for (g, hw, table, L, order[, batched splits]); `order`
@@ -387,7 +407,8 @@ def get_plan(g, hw, table, L: int, order: Optional[Sequence[str]] = None,
             order = None
     if batched is not None:
         batched = tuple(sorted(set(int(x) for x in batched)))
-    key = (id(g), id(hw), id(table), int(L), order, batched)
+    key = (id(g), id(hw), id(table), int(L), order, batched,
+           _fingerprint(g, hw, table))
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None:
