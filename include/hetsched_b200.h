@@ -27,6 +27,10 @@
  *                      transitive_closure core.py:104-111 as bitsets.
  *   hs_best_merge   -- (no reference counterpart) lexicographic
  *                      (cost, index) merge of per-rank bests.
+ *   hs_best_allreduce -- the same merge across GPUs over NCCL.
+ *   hs_bridges_articulation / hs_k_edge_components -- module detection,
+ *                      splitting.py:36-81, 178-219.
+ *   hs_validate_schedules -- validate_schedule core.py:206-291, batched.
  */
 #ifndef HETSCHED_B200_H
 #define HETSCHED_B200_H
@@ -265,6 +269,92 @@ int hs_modularity(const hs_plan *plan, const int32_t *d_labels, int64_t P,
 
 /* host: lexicographic (cost, index) minimum of n bests */
 int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out);
+
+/* Module detection of the split heuristic (host, one-time per graph; no
+ * device work). Graph = n_tasks tasks (insertion order) and n_edges directed
+ * edges; both work on the undirected shadow (splitting.py:28-33).
+ *
+ * hs_bridges_articulation -- find_bridges_and_articulation_points
+ *   (splitting.py:36-81): is_bridge[e] = 1 when edge e (either orientation)
+ *   is a bridge, is_articulation[v] = 1 for cut vertices, *connected = 1
+ *   when the shadow is connected. Any output may be NULL.
+ * hs_k_edge_components -- k_edge_components(g, c) (splitting.py:178-219)
+ *   with k = c + 1: module_of[v] = the module index of task v, modules being
+ *   the k-edge-connected components of the shadow (networkx semantics:
+ *   maximal sets with pairwise edge connectivity >= k), cycles of the module
+ *   digraph merged, numbered by the lexicographic topological order keyed
+ *   by each module's smallest task id (UTF-8 bytes, = Python str order). */
+int hs_bridges_articulation(int32_t n_tasks, int32_t n_edges, const int32_t *edge_src,
+                            const int32_t *edge_dst, uint8_t *is_bridge,
+                            uint8_t *is_articulation, int32_t *connected);
+int hs_k_edge_components(int32_t n_tasks, const char *task_ids,
+                         const int64_t *task_id_off, int32_t n_edges,
+                         const int32_t *edge_src, const int32_t *edge_dst, int32_t k,
+                         int32_t *module_of, int32_t *n_modules);
+
+/* Schedule validation on the GPU (K11): validate_schedule core.py:206-291
+ * for n_sched schedules in one call (one CTA each). The instance is a
+ * description as for hs_plan_create (L and order are ignored; latency holds
+ * every (device, batch size) column). Schedule q owns batches
+ * [h_batch_off[q], h_batch_off[q+1]) in its own order, input values
+ * h_inputs[in_off .. in_off + n_inputs), input_count h_input_count[q] and
+ * stated objective h_objective[q]. h_out[q] receives the FIRST violation in
+ * the reference's check order (code 0 = valid, v0 = makespan), with the
+ * indices / values its message needs; all buffers are host memory. */
+typedef struct hs_sched_batch {
+    int32_t task;       /* task insertion index, -1 = not in the graph    */
+    int32_t device;     /* device insertion index, -1 = unknown device    */
+    int32_t size;       /* b.size (-1 if outside int32)                   */
+    int32_t n_inputs;   /* len(b.inputs)                                  */
+    int64_t in_off;     /* first input value in h_inputs                  */
+    double start;       /* b.start                                        */
+    int32_t flags;      /* bit 0: b.inputs repeats a value                */
+    int32_t pad;
+} hs_sched_batch;
+
+typedef struct hs_violation {
+    int32_t code;       /* HS_V_*                                          */
+    int32_t a, b, c;    /* batch / task / edge / device indices, see codes */
+    double v0, v1, v2;  /* values of the message (v0 = makespan if valid)  */
+} hs_violation;
+
+#define HS_V_OK 0
+#define HS_V_UNKNOWN_TASK 1    /* a = batch                                 */
+#define HS_V_UNKNOWN_DEVICE 2  /* a = batch                                 */
+#define HS_V_SIZE 3            /* a = batch: size vs inputs                 */
+#define HS_V_BATCH_SIZE 4      /* a = batch: size not supported by device   */
+#define HS_V_NEGATIVE_START 5  /* a = batch                                 */
+#define HS_V_INPUT_RANGE 6     /* a = batch, c = position in its inputs     */
+#define HS_V_DOUBLE 7          /* a = batch, c = position: assigned twice   */
+#define HS_V_LATENCY 8         /* a = batch: missing entry (GraphError)     */
+#define HS_V_UNASSIGNED 9      /* a = task, c = input (1-based)             */
+#define HS_V_NO_LINK 10        /* a = edge, b = producer batch, c = input   */
+#define HS_V_PRECEDENCE 11     /* a = edge, b = producer batch, c = input;
+                                  v0 = consumer start, v1 = producer end,
+                                  v2 = comm                                 */
+#define HS_V_OVERLAP 12        /* a, b = batches (sorted order), c = device;
+                                  v0, v1 = their ends                       */
+#define HS_V_MEMORY 13         /* a = device, v0 = used, v1 = memory        */
+#define HS_V_OBJECTIVE 14      /* v0 = makespan, v1 = stated objective      */
+
+int hs_validate_schedules(const hs_instance_desc *desc, int64_t n_sched,
+                          const int64_t *h_batch_off, const hs_sched_batch *h_batches,
+                          const int64_t *h_inputs, const int32_t *h_input_count,
+                          const double *h_objective, double tol, hs_violation *h_out,
+                          void *stream);
+
+/* Multi-GPU: the global best over every rank of an NCCL communicator. Each
+ * rank passes its device-resident local best (hs_eval's d_best, indices
+ * already global through index_base); d_out (device) receives the
+ * lexicographic (cost, index) minimum on every rank. One ncclAllGather of
+ * 16 B per rank on `stream` plus a one-thread merge kernel (NCCL has no
+ * argmin operator). NCCL is bound at run time
+ * (dlopen("libnccl.so.2")), so `comm` must come from the NCCL already loaded
+ * in the process (e.g. torch's ProcessGroupNCCL._comm_ptr()). No reference
+ * counterpart: the reference runs on one host and never reduces. */
+struct ncclComm;
+int hs_best_allreduce(const hs_best *d_in, hs_best *d_out, struct ncclComm *comm,
+                      void *stream);
 
 #ifdef __cplusplus
 }

@@ -21,9 +21,12 @@ from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
                          specialize, throughput)
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
                      dep_subgraph, lower_bound, pre_subgraph)
-from .splitting import ModuleSolver, gpu_module_solver
+from .splitting import (ModuleDecomposition, ModuleSolver,
+                        find_bridges_and_articulation_points,
+                        gpu_module_solver, k_edge_components, milp_split)
 from .batched import (batched_genes_from_schedule, batched_options,
                       decode_batched, fitness_batched, random_search_batched)
+from .validate import validate_schedule, validate_schedules
 from .modularity import (decomposition_modularity, modularity,
                          modularity_batch)
 

@@ -114,6 +114,14 @@ def load() -> C.CDLL:
             "hs_modularity": (C.c_int, [vp, vp, i64, i32, C.c_double, vp, vp,
                                         vp]),
             "hs_best_merge": (C.c_int, [_p(Best), i64, _p(Best)]),
+            "hs_best_allreduce": (C.c_int, [vp, vp, vp, vp]),
+            "hs_bridges_articulation": (C.c_int, [i32, i32, vp, vp, vp, vp,
+                                                  vp]),
+            "hs_k_edge_components": (C.c_int, [i32, C.c_char_p, vp, i32, vp,
+                                               vp, i32, vp, vp]),
+            "hs_validate_schedules": (C.c_int, [_p(InstanceDesc), i64, vp, vp,
+                                                vp, vp, vp, C.c_double, vp,
+                                                vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -134,7 +142,9 @@ def exported_symbols() -> list[str]:
             "hs_eval_host", "hs_eval_packed", "hs_eval_host_packed",
             "hs_eval_packed3", "hs_eval_host_packed3", "hs_ea_run",
             "hs_ea_run_chunk", "hs_sa_run", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
-            "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge"]
+            "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge",
+            "hs_best_allreduce", "hs_bridges_articulation",
+            "hs_k_edge_components", "hs_validate_schedules"]
 
 
 def check(rc: int, what: str = "") -> None:

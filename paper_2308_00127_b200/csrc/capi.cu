@@ -52,6 +52,10 @@ uint32_t flags_of(const hs::Plan &p) {
 
 namespace hs {
 
+// the thread-local error message of hs_last_error(), for the other
+// translation units of the library (decomp.cpp, validate.cu)
+int set_error(int code, const std::string &msg) { return set_err(code, msg); }
+
 Plan::~Plan() {
     int cur = -1;
     cudaGetDevice(&cur);
@@ -945,3 +949,90 @@ int hs_best_merge(const hs_best *bests, int64_t n, hs_best *out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU best: one NCCL all-gather of 16 B per rank + an on-device
+// lexicographic merge (NCCL has no argmin operator). NCCL is
+// resolved at run time with dlopen("libnccl.so.2"): when the caller's NCCL is
+// already in the process (torch's, or the application's) the loader returns
+// that very library, so the communicator handed in is always used with the
+// NCCL that created it, and the library carries no link-time NCCL dependency.
+#include <dlfcn.h>
+
+#include <mutex>
+
+namespace {
+
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, ncclComm *,
+                                 cudaStream_t);
+typedef int (*nccl_count_fn)(const ncclComm *, int *);
+typedef const char *(*nccl_errstr_fn)(int);
+constexpr int kNcclInt64 = 4;  // ncclInt64 in nccl.h's ncclDataType_t
+
+struct NcclApi {
+    nccl_allgather_fn allgather = nullptr;
+    nccl_count_fn count = nullptr;
+    nccl_errstr_fn errstr = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+const NcclApi &nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.why = std::string("dlopen libnccl.so.2: ") + dlerror();
+            return;
+        }
+        api.allgather = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+        api.count = reinterpret_cast<nccl_count_fn>(dlsym(h, "ncclCommCount"));
+        api.errstr = reinterpret_cast<nccl_errstr_fn>(dlsym(h, "ncclGetErrorString"));
+        api.ok = api.allgather && api.count;
+        if (!api.ok) api.why = "libnccl.so.2 lacks ncclAllGather / ncclCommCount";
+    });
+    return api;
+}
+
+// the same rule as hs_best_merge, on the device, over the gathered ranks
+__global__ void best_merge_kernel(const hs_best *in, int n, hs_best *out) {
+    if (threadIdx.x != 0) return;
+    hs_best b{__longlong_as_double(0x7FF0000000000000LL), -1};
+    for (int k = 0; k < n; ++k) {
+        const hs_best c = in[k];
+        if (c.index < 0) continue;
+        if (b.index < 0 || c.cost < b.cost || (c.cost == b.cost && c.index < b.index))
+            b = c;
+    }
+    *out = b;
+}
+
+}  // namespace
+
+extern "C" int hs_best_allreduce(const hs_best *d_in, hs_best *d_out, ncclComm *comm,
+                                 void *stream) {
+    if (!d_in || !d_out || !comm) return set_err(HS_EINVAL, "null argument");
+    const NcclApi &api = nccl_api();
+    if (!api.ok) return set_err(HS_ECUDA, api.why);
+    int nranks = 0;
+    int nr = api.count(comm, &nranks);
+    if (nr != 0 || nranks < 1)
+        return set_err(HS_ECUDA, std::string("ncclCommCount: ") +
+                                     (api.errstr ? api.errstr(nr) : "failed"));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    hs_best *all = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&all), sizeof(hs_best) * size_t(nranks), s));
+    nr = api.allgather(d_in, all, 2, kNcclInt64, comm, s);
+    if (nr != 0) {
+        cudaFreeAsync(all, s);
+        return set_err(HS_ECUDA, std::string("ncclAllGather: ") +
+                                     (api.errstr ? api.errstr(nr) : "failed"));
+    }
+    best_merge_kernel<<<1, 32, 0, s>>>(all, nranks, d_out);
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(all, s);
+    if (e != cudaSuccess) return cuda_err(e, "best_merge_kernel");
+    return HS_OK;
+}

@@ -56,6 +56,38 @@ def allgather_best(best: tuple[float, int], group=None,
     return merge_best([(float(costs[r]), int(o[r, 1])) for r in range(world)])
 
 
+def nccl_comm(group=None) -> int:
+    """The ncclComm_t (as an int) of torch's NCCL process group on the
+    current device. Initialise the group eagerly (``init_process_group(...,
+    device_id=...)``) so the communicator exists."""
+    import torch
+    import torch.distributed as dist
+    pg = group if group is not None else \
+        dist.distributed_c10d._get_default_group()
+    be = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+    ptr = int(be._comm_ptr())
+    if not ptr:
+        raise RuntimeError("NCCL communicator not initialised")
+    return ptr
+
+
+def best_allreduce_device(best, out, comm: int, stream=None) -> None:
+    """hs_best_allreduce: `best` int64[2] device tensor (cost bits, global
+    index; hs_eval's fused argmin) -> `out` int64[2], the lexicographic
+    minimum over every rank of `comm` (one ncclAllGather of 16 B per rank
+    and an on-device merge, all on `stream`)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+    s = stream if stream is not None else torch.cuda.current_stream()
+    N.check(N.load().hs_best_allreduce(
+        C.c_void_p(best.data_ptr()), C.c_void_p(out.data_ptr()),
+        C.c_void_p(comm), C.c_void_p(int(s.cuda_stream))),
+        "hs_best_allreduce")
+
+
 def sharded_best(n: int, evaluate: Callable[[int, int], tuple[float, int]],
                  group=None, device: Optional[str] = None) -> tuple[float, int]:
     """Evaluate this rank's shard with `evaluate(lo, hi) -> (cost, global

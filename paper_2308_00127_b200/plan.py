@@ -48,6 +48,64 @@ def _strings(ids):
     return b"".join(raw), off
 
 
+def instance_desc(g, hw, table, L: int = 1,
+                  order: Optional[Sequence[str]] = None):
+    """The C ABI's hs_instance_desc of (g, hw, table, L[, genome order]) and
+    the Python objects that must stay alive while it is used (the last
+    three: task ids, device ids, latency column list)."""
+    task_ids = list(g.tasks)
+    tix = {t: k for k, t in enumerate(task_ids)}
+    dev_ids = list(hw.devices)
+    K = len(dev_ids)
+    tnodes = [g.tasks[t] for t in task_ids]
+    wm = np.array([float(t.wm) for t in tnodes], np.float64)
+    im = np.array([float(t.im) for t in tnodes], np.float64)
+    om = np.array([float(t.om) for t in tnodes], np.float64)
+    src = np.array([tix[a] for a, _ in g.edges], np.int32)
+    dst = np.array([tix[b] for _, b in g.edges], np.int32)
+    devs = [hw.devices[u] for u in dev_ids]
+    memory = np.array([float(d.memory) for d in devs], np.float64)
+    sizes = [tuple(int(b) for b in d.batch_sizes) for d in devs]
+    boff = np.zeros(K + 1, np.int32)
+    boff[1:] = np.cumsum([len(s) for s in sizes])
+    bs = np.array([b for s in sizes for b in s], np.int32)
+    bw = np.zeros((K, K), np.float64)
+    dix = {u: k for k, u in enumerate(dev_ids)}
+    for (a, b), v in hw.bandwidth.items():
+        bw[dix[a], dix[b]] = float(v)
+    cols = [(u, b) for u, s in zip(dev_ids, sizes) for b in s]
+    ent = table.entries
+    lat = np.zeros((len(task_ids), max(len(cols), 1)), np.float64)
+    ok = np.zeros(lat.shape, np.uint8)
+    for r, t in enumerate(task_ids):
+        for c, (u, b) in enumerate(cols):
+            v = ent.get((t, u, b))
+            if v is not None:
+                lat[r, c] = v
+                ok[r, c] = 1
+    tid_bytes, toff = _strings(task_ids)
+    did_bytes, doff = _strings(dev_ids)
+    order_arr = None
+    if order is not None:
+        try:
+            order_arr = np.array([tix[t] for t in order], np.int32)
+        except KeyError as exc:
+            raise GraphError(f"genome order names unknown task {exc}")
+        if len(order_arr) != len(task_ids):
+            raise GraphError("genome length must equal task count")
+    keep = (wm, im, om, src, dst, memory, boff, bs, bw, lat, ok, tid_bytes,
+            toff, did_bytes, doff, order_arr, task_ids, dev_ids, cols)
+    d = N.InstanceDesc(
+        n_tasks=len(task_ids), task_ids=tid_bytes, task_id_off=_i64(toff),
+        wm=_f64(wm), im=_f64(im), om=_f64(om),
+        n_edges=len(src), edge_src=_i32(src), edge_dst=_i32(dst),
+        n_devices=K, dev_ids=did_bytes, dev_id_off=_i64(doff),
+        memory=_f64(memory), batch_off=_i32(boff), batch_sizes=_i32(bs),
+        bandwidth=_f64(bw), L=int(L), latency=_f64(lat), latency_ok=_u8(ok),
+        order=_i32(order_arr) if order_arr is not None else None)
+    return d, keep
+
+
 class Plan:
     """Native evaluation plan of one instance at load L."""
 
@@ -58,57 +116,9 @@ class Plan:
         reference's default L/4, L/2, 3L/4, L) makes a batched-variant plan
         whose genes are option indices (heuristics.py:337-433)."""
         lib = N.load()
-        task_ids = list(g.tasks)
-        tix = {t: k for k, t in enumerate(task_ids)}
-        dev_ids = list(hw.devices)
-        K = len(dev_ids)
-        tnodes = [g.tasks[t] for t in task_ids]
-        wm = np.array([float(t.wm) for t in tnodes], np.float64)
-        im = np.array([float(t.im) for t in tnodes], np.float64)
-        om = np.array([float(t.om) for t in tnodes], np.float64)
-        src = np.array([tix[a] for a, _ in g.edges], np.int32)
-        dst = np.array([tix[b] for _, b in g.edges], np.int32)
-        devs = [hw.devices[u] for u in dev_ids]
-        memory = np.array([float(d.memory) for d in devs], np.float64)
-        sizes = [tuple(int(b) for b in d.batch_sizes) for d in devs]
-        boff = np.zeros(K + 1, np.int32)
-        boff[1:] = np.cumsum([len(s) for s in sizes])
-        bs = np.array([b for s in sizes for b in s], np.int32)
-        bw = np.zeros((K, K), np.float64)
-        for (a, b), v in hw.bandwidth.items():
-            bw[dev_ids.index(a), dev_ids.index(b)] = float(v)
-        cols = [(u, b) for u, s in zip(dev_ids, sizes) for b in s]
-        ent = table.entries
-        lat = np.zeros((len(task_ids), max(len(cols), 1)), np.float64)
-        ok = np.zeros(lat.shape, np.uint8)
-        for r, t in enumerate(task_ids):
-            for c, (u, b) in enumerate(cols):
-                v = ent.get((t, u, b))
-                if v is not None:
-                    lat[r, c] = v
-                    ok[r, c] = 1
-        tid_bytes, toff = _strings(task_ids)
-        did_bytes, doff = _strings(dev_ids)
-        order_arr = None
-        if order is not None:
-            try:
-                order_arr = np.array([tix[t] for t in order], np.int32)
-            except KeyError as exc:
-                raise GraphError(f"genome order names unknown task {exc}")
-            if len(order_arr) != len(task_ids):
-                raise GraphError("genome length must equal task count")
-        # keep every buffer alive for the duration of the call
-        self._keep = (wm, im, om, src, dst, memory, boff, bs, bw, lat, ok,
-                      tid_bytes, toff, did_bytes, doff, order_arr)
-        d = N.InstanceDesc(
-            n_tasks=len(task_ids), task_ids=tid_bytes, task_id_off=_i64(toff),
-            wm=_f64(wm), im=_f64(im), om=_f64(om),
-            n_edges=len(src), edge_src=_i32(src), edge_dst=_i32(dst),
-            n_devices=K, dev_ids=did_bytes, dev_id_off=_i64(doff),
-            memory=_f64(memory), batch_off=_i32(boff), batch_sizes=_i32(bs),
-            bandwidth=_f64(bw), L=int(L), latency=_f64(lat),
-            latency_ok=_u8(ok),
-            order=_i32(order_arr) if order_arr is not None else None)
+        d, keep = instance_desc(g, hw, table, L, order)
+        self._keep = keep
+        task_ids, dev_ids, K = keep[-3], keep[-2], d.n_devices
         if K == 0:
             raise GraphError("gene value out of device range")
         h = C.c_void_p()

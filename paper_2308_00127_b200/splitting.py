@@ -1,31 +1,142 @@
-"""GPU module solver for the split heuristic (MILP-SPLIT).
+"""The split heuristic (MILP-SPLIT) on the B200 path: module detection,
+the GPU module solver, and the dynamic program that combines them.
 
-The reference's ``milp_split`` (/root/reference/pkg/src/hetsched/
-splitting.py:259-402) solves every module once per pinning of its channel
-endpoints through a pluggable ``ModuleSolver`` (splitting.py:225), called as
-``solver(sub, hw, table, L, pins, same_device, timeout)`` and returning
-``(objective, schedule, proven_optimal)`` or ``(None, None, False)``
-(splitting.py:228-245, 338-340). ``gpu_module_solver`` is a drop-in for that
-slot: it sweeps the module's mappings on the B200 -- exhaustively when the
-free assignments number at most ``exhaustive_limit``, otherwise by on-device
-random sampling followed by batched best-improvement 1-opt -- with pinned
-tasks fixed and ``same_device`` pairs tied (milp.py:277-291), and returns the
-decoded schedule of the best mapping. The objective is the list-scheduling
-makespan, so ``proven_optimal`` is False (optimal over decoder mappings, not
-a MILP certificate); the reference DP then flags the result quasi-optimal.
-It is thread-safe (the DP may call it from a thread pool).
+* ``find_bridges_and_articulation_points`` / ``k_edge_components``
+  (reference splitting.py:36-81, 178-219) run natively (csrc/decomp.cpp,
+  C ABI ``hs_bridges_articulation`` / ``hs_k_edge_components``) and return
+  the reference's ``ModuleDecomposition`` shape (modules in the same
+  lexicographic topological order, cut edges in edge order).
+* ``gpu_module_solver`` fills the reference's pluggable ``ModuleSolver``
+  slot (splitting.py:225), called as ``solver(sub, hw, table, L, pins,
+  same_device, timeout)`` and returning ``(objective, schedule,
+  proven_optimal)`` or ``(None, None, False)`` (splitting.py:228-245,
+  338-340). It sweeps the module's mappings on the B200 -- exhaustively when
+  the free assignments number at most ``exhaustive_limit``, otherwise by
+  on-device random sampling followed by batched best-improvement 1-opt --
+  with pinned tasks fixed and ``same_device`` pairs tied (milp.py:277-291),
+  and returns the decoded schedule of the best mapping. The objective is the
+  list-scheduling makespan, so ``proven_optimal`` is False (optimal over
+  decoder mappings, not a MILP certificate); the DP then flags the result
+  quasi-optimal. It is thread-safe (the DP may call it from a thread pool).
+* ``milp_split`` is the reference's DP over channel-endpoint device pinnings
+  (splitting.py:259-402) with the same states, tie rules and flags; its
+  default module solver here is ``gpu_module_solver`` (this package has no
+  MILP: the reference's ``default_module_solver`` stays a CPU consumer that
+  can be passed in).
 """
 from __future__ import annotations
 
+import ctypes as C
+import itertools
+import json
 import time
-from typing import Callable, Optional
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
 from . import _native as N
-from .core import Schedule
+from .core import GraphError, Schedule, ScheduledBatch, ScheduleError
 from .heuristics import MappingGenome, decode, _fit_rows
-from .plan import get_plan
+from .plan import _strings, get_plan
+
+MAX_PIN_TASKS = 4
+
+
+# ---------------------------------------------------------------------------
+# module detection (native)
+
+def _edge_arrays(g):
+    ids = list(g.tasks)
+    tix = {t: k for k, t in enumerate(ids)}
+    src = np.array([tix[a] for a, _ in g.edges], np.int32)
+    dst = np.array([tix[b] for _, b in g.edges], np.int32)
+    return ids, src, dst
+
+
+def find_bridges_and_articulation_points(g):
+    """(bridges in edge order and orientation, articulation set, connected)
+    of the undirected shadow (reference splitting.py:36-81)."""
+    lib = N.load()
+    ids, src, dst = _edge_arrays(g)
+    br = np.zeros(max(len(src), 1), np.uint8)
+    art = np.zeros(max(len(ids), 1), np.uint8)
+    conn = C.c_int32()
+    N.check(lib.hs_bridges_articulation(
+        len(ids), len(src), src.ctypes.data, dst.ctypes.data, br.ctypes.data,
+        art.ctypes.data, C.byref(conn)), "hs_bridges_articulation")
+    bridges = [e for e, b in zip(g.edges, br) if b]
+    return bridges, {t for t, a in zip(ids, art) if a}, bool(conn.value)
+
+
+@dataclass
+class ModuleDecomposition:
+    """Same shape and methods as the reference's (splitting.py:134-175)."""
+    modules: list  # topologically ordered partition of V (frozensets)
+    cut_edges: dict  # (from module, to module) -> [(src, dst)] edge order
+    channels: int
+    is_chain: bool
+
+    def module_of(self) -> dict:
+        return {t: k for k, mod in enumerate(self.modules) for t in mod}
+
+    def in_edges(self, t: int) -> list:
+        return [(a, e) for (a, b), es in self.cut_edges.items() if b == t
+                for e in es]
+
+    def max_cut_width(self) -> int:
+        return max((len(e) for e in self.cut_edges.values()), default=0)
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "channels": self.channels, "is_chain": self.is_chain,
+            "modules": [sorted(m) for m in self.modules],
+            "cuts": [{"from": a, "to": b, "edges": [list(e) for e in es]}
+                     for (a, b), es in sorted(self.cut_edges.items())],
+        }, indent=2) + "\n"
+
+    @classmethod
+    def from_json(cls, text: str) -> "ModuleDecomposition":
+        doc = json.loads(text)
+        try:
+            return cls(modules=[frozenset(m) for m in doc["modules"]],
+                       cut_edges={(int(c["from"]), int(c["to"])):
+                                  [(e[0], e[1]) for e in c["edges"]]
+                                  for c in doc["cuts"]},
+                       channels=int(doc["channels"]),
+                       is_chain=bool(doc["is_chain"]))
+        except (KeyError, TypeError, IndexError) as exc:
+            raise GraphError(f"bad decomposition document: {exc}") from exc
+
+
+def k_edge_components(g, c: int = 1) -> ModuleDecomposition:
+    """Modules = (c+1)-edge-connected components of the undirected shadow,
+    cycles merged, in the reference's lexicographic topological order
+    (splitting.py:178-219); computed by hs_k_edge_components."""
+    if c < 1:
+        raise GraphError("channel budget c must be >= 1")
+    lib = N.load()
+    ids, src, dst = _edge_arrays(g)
+    raw, off = _strings(ids)
+    mod = np.zeros(max(len(ids), 1), np.int32)
+    nm = C.c_int32()
+    N.check(lib.hs_k_edge_components(
+        len(ids), raw, off.ctypes.data, len(src), src.ctypes.data,
+        dst.ctypes.data, int(c) + 1, mod.ctypes.data, C.byref(nm)),
+        "hs_k_edge_components")
+    groups: list = [[] for _ in range(nm.value)]
+    for t, m in zip(ids, mod):
+        groups[m].append(t)
+    module_of = dict(zip(ids, (int(m) for m in mod)))
+    cuts: dict = {}
+    for a, b in g.edges:
+        ma, mb = module_of[a], module_of[b]
+        if ma != mb:
+            cuts.setdefault((ma, mb), []).append((a, b))
+    return ModuleDecomposition(
+        modules=[frozenset(x) for x in groups], cut_edges=cuts, channels=c,
+        is_chain=all(b == a + 1 for (a, b) in cuts))
 
 ModuleSolver = Callable[..., tuple[Optional[float], Optional[Schedule], bool]]
 
@@ -156,3 +267,135 @@ def _refine(plan, genes, cost, group, K, rounds, deadline):
         if deadline is not None and time.monotonic() > deadline:
             break
     return genes, cost
+
+
+# ---------------------------------------------------------------------------
+# the split DP (reference splitting.py:248-402)
+
+def _met_device(task, hw, table, L: int) -> str:
+    """Fastest device for a task at L (or its smallest batch size), ties to
+    the smaller id (splitting.py:248-256)."""
+    pick = None
+    for u in sorted(hw.devices):
+        sizes = hw.devices[u].batch_sizes
+        ms = table.get(task, u, L if L in sizes else sizes[0])
+        if pick is None or ms < pick[0] - 1e-12:
+            pick = (ms, u)
+    return pick[1]
+
+
+def milp_split(g, hw, table, L: int, decomposition: ModuleDecomposition,
+               module_solver: Optional[ModuleSolver] = None,
+               timeout: Optional[float] = None, objective: str = "latency",
+               same_device: Optional[Sequence[tuple]] = None,
+               max_pins: int = MAX_PIN_TASKS,
+               workers: Optional[int] = None) -> Schedule:
+    """Solve every module once per device pinning of its live channel
+    endpoints and chain the solutions: cost(module t, pins) = cost of the
+    predecessor state + the slowest incoming channel transfer + the module's
+    objective, kept per live-endpoint state, first strict improvement by
+    more than 1e-12 wins (splitting.py:259-402). Same flags, states and
+    assembly as the reference; `module_solver` defaults to the GPU sweep."""
+    solver = module_solver if module_solver is not None \
+        else gpu_module_solver(objective)
+    pairs = list(same_device or ())
+    mods = decomposition.modules
+    T = len(mods)
+    width = decomposition.max_cut_width()
+    flags: set = set()
+    if width > 1:
+        flags.add("multi-channel")
+    if not decomposition.is_chain:
+        flags.add("non-chain")
+    if L > 1 and width > 1:
+        flags.add("quasi-optimal")
+    devs = sorted(hw.devices)
+    # with every pair linked a zero-byte transfer is free wherever its ends
+    # sit, so such a channel needs no pinning
+    mesh = all((u, v) in hw.bandwidth for u in devs for v in devs if u != v)
+
+    def pinned(src) -> bool:
+        return g.tasks[src].om > 0 or not mesh
+
+    outs: list = [[] for _ in range(T)]   # live sources leaving module t
+    ins: list = [[] for _ in range(T)]    # channel targets inside module t
+    last: dict = {}                       # last module reading a source
+    for (a, b), es in decomposition.cut_edges.items():
+        for src, dst in es:
+            if not pinned(src):
+                continue
+            if src not in outs[a]:
+                outs[a].append(src)
+            if dst not in ins[b]:
+                ins[b].append(dst)
+            last[src] = max(last.get(src, -1), b)
+    subs = [g.subgraph(m, name=f"module{t}") for t, m in enumerate(mods)]
+
+    def combos(tasks: list):
+        if len(tasks) > max_pins:
+            flags.update(("quasi-optimal", "heuristic-pinning"))
+            yield {t: _met_device(t, hw, table, L) for t in tasks}
+            return
+        for assign in itertools.product(devs, repeat=len(tasks)):
+            pins = dict(zip(tasks, assign))
+            if all(not (a in pins and b in pins and pins[a] != pins[b])
+                   for a, b in pairs):
+                yield pins
+
+    def solve_all(t: int) -> dict:
+        choices = list(combos(sorted(set(ins[t]) | set(outs[t]))))
+        local = [(a, b) for a, b in pairs if a in mods[t] and b in mods[t]]
+
+        def one(pins):
+            return solver(subs[t], hw, table, L, pins, local, timeout)
+
+        if workers and workers > 1 and len(choices) > 1:
+            with ThreadPoolExecutor(max_workers=workers) as ex:
+                res = list(ex.map(one, choices))
+        else:
+            res = [one(p) for p in choices]
+        table_t = {}
+        for pins, (obj, sched, exact) in zip(choices, res):
+            if obj is None:
+                continue
+            if not exact:
+                flags.add("quasi-optimal")
+            table_t[tuple(sorted(pins.items()))] = (obj, sched, pins)
+        return table_t
+
+    states: dict = {(): (0.0, [])}
+    for t in range(T):
+        solved = solve_all(t)
+        if not solved and mods[t]:
+            raise ScheduleError(f"no feasible pinning for module {t}")
+        incoming = [e for _a, e in decomposition.in_edges(t) if pinned(e[0])]
+        nxt: dict = {}
+        for state, (cost, trail) in sorted(states.items()):
+            held = dict(state)
+            for _key, (obj, sched, pins) in sorted(solved.items()):
+                delay, ok = 0.0, True
+                for src, dst in incoming:
+                    c = hw.comm_time(g.tasks[src].om, held[src], pins[dst])
+                    if c is None:
+                        ok = False
+                        break
+                    delay = max(delay, c)
+                if not ok:
+                    continue
+                total = cost + delay + obj
+                keep = {s: d for s, d in held.items() if last[s] > t}
+                keep.update({s: pins[s] for s in outs[t] if last[s] > t})
+                key = tuple(sorted(keep.items()))
+                cur = nxt.get(key)
+                if cur is None or total < cur[0] - 1e-12:
+                    nxt[key] = (total, trail + [(t, sched, cost + delay)])
+        if not nxt:
+            raise ScheduleError(f"no feasible pinning for module {t} "
+                                "(missing links)")
+        states = nxt
+    total, trail = states[min(states, key=lambda k: states[k][0])]
+    batches = [ScheduledBatch(task=b.task, device=b.device, size=b.size,
+                              inputs=b.inputs, start=b.start + off)
+               for _t, sched, off in trail for b in sched.batches]
+    return Schedule(batches=tuple(batches), objective=total, input_count=L,
+                    flags=tuple(sorted(flags)))
