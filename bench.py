@@ -278,10 +278,14 @@ def _spawn_ranks(args):
     status; the ranks then find WORLD_SIZE == N."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
         return
+    # torchrun's parser prefix-matches every "--x" token, so pass the
+    # ambiguous alias --n under its full name
+    argv = ["--candidates" + a[3:] if a == "--n" or a.startswith("--n=")
+            else a for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
            "--master-port", str(_free_port()), os.path.abspath(__file__),
-           *sys.argv[1:]]
+           *argv]
     sys.exit(subprocess.call(cmd))
 
 
@@ -560,8 +564,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 24,
-                    help="candidates per GPU per step")
+    ap.add_argument("--candidates", "--n", dest="n", type=int,
+                    default=1 << 24, help="candidates per GPU per step")
     ap.add_argument("--e2e-n", type=int, default=1 << 23)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tts", action="store_true")

@@ -8,15 +8,20 @@ drop-in for ``hetsched.bounds`` (/root/reference/pkg/src/hetsched/bounds.py).
 * ``lower_bound`` (bounds.py:142-236) is the same recursion and the same
   ``terms`` report; every critical path a level needs is computed in one
   batched launch (the reference's ``prefetch`` points). Subgraphs of at most
-  ``subgraph_cap`` tasks are solved exactly by a MILP callable -- by default
-  the reference's own ``hetsched.milp`` when it is importable (branch and
-  bound stays on the CPU); without one, the bound uses the
-  critical path for every subgraph (the reference's ``subgraph_cap=0``).
+  ``subgraph_cap`` tasks are solved exactly by an explicit MILP sub-solver
+  (``milp=``; branch and bound stays on the CPU), run
+  ``workers`` at a time in a thread pool at every prefetch point like the
+  reference's ``_SubgraphOpt.prefetch`` (bounds.py:126-131). Left at its
+  default, ``milp`` is the reference's own MILP (``hetsched.milp``) when that
+  package is installed; with ``subgraph_cap > 0`` and no sub-solver the call
+  raises instead of quietly using critical paths (which is what
+  ``subgraph_cap=0`` asks for).
 """
 from __future__ import annotations
 
 import json
 import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -135,8 +140,9 @@ class BoundReport:
 
 
 def reference_milp_solver() -> Optional[Callable]:
-    """Exact sub-solver backed by the reference's MILP (milp.py:137-494)
-    when ``hetsched`` is importable, else None."""
+    """Exact sub-solver backed by the reference's MILP (milp.py:137-494):
+    ``solve(sub, hw, table, load, timeout) -> (status, objective,
+    dual_bound)``; None when ``hetsched`` is not installed."""
     try:
         from hetsched import milp as milp_mod  # type: ignore
     except Exception:
@@ -151,12 +157,14 @@ def reference_milp_solver() -> Optional[Callable]:
 
 
 class _SubgraphValues:
-    """OPT or a valid lower bound per (task set, load), memoised; the
-    critical paths of a prefetch list are one GPU launch."""
+    """OPT or a valid lower bound per (task set, load), memoised
+    (bounds.py:91-131); the critical paths of a prefetch list are one GPU
+    launch and its MILP sub-solves run `workers` at a time."""
 
-    def __init__(self, g, hw, table, timeout, cap, milp):
+    def __init__(self, g, hw, table, timeout, cap, milp, workers):
         self.g, self.hw, self.table = g, hw, table
         self.timeout, self.cap, self.milp = timeout, cap, milp
+        self.workers = workers
         self.cache: dict = {}
         self.cp: dict = {}
 
@@ -169,6 +177,16 @@ class _SubgraphValues:
             for t, v in zip(todo, critical_path_bounds(
                     self.g, self.hw, self.table, todo)):
                 self.cp[t] = v
+        if self.milp is None or not self.workers or self.workers < 2:
+            return
+        solve = []
+        for it in items:
+            if it[0] and len(it[0]) <= self.cap and it not in self.cache \
+                    and it not in solve:
+                solve.append(it)
+        if len(solve) > 1:
+            with ThreadPoolExecutor(max_workers=self.workers) as ex:
+                list(ex.map(lambda it: self.value(*it), solve))
 
     def value(self, tasks: frozenset, load: int):
         if not tasks:
@@ -177,9 +195,10 @@ class _SubgraphValues:
         hit = self.cache.get(key)
         if hit is not None:
             return hit
-        self.prefetch([key])
+        if tasks not in self.cp:
+            self.prefetch([key])
         cp = self.cp[tasks]
-        if len(tasks) > self.cap or self.milp is None:
+        if len(tasks) > self.cap:
             out = (cp, "critical-path")
         else:
             sub = self.g.subgraph(tasks)
@@ -191,6 +210,8 @@ class _SubgraphValues:
                 raise GraphError(f"subgraph of {len(tasks)} tasks infeasible "
                                  f"at load {load}")
             else:
+                # an incumbent is no lower bound: the solver's dual bound,
+                # floored by the critical path
                 out = (max(cp, dual if dual is not None else 0.0),
                        "dual-bound")
         self.cache[key] = out
@@ -211,10 +232,20 @@ def lower_bound(g, hw, table, L: int, decomposition,
                 workers: Optional[int] = None,
                 milp: Optional[Callable] = ...) -> BoundReport:
     """max of the two paper inequalities at every cut, recursively
-    (bounds.py:142-236); see the module docstring for the sub-solver."""
-    if milp is ...:
-        milp = reference_milp_solver() if subgraph_cap > 0 else None
-    vals = _SubgraphValues(g, hw, table, timeout, subgraph_cap, milp)
+    (bounds.py:142-236); see the module docstring for the sub-solver.
+    `milp(sub, hw, table, load, timeout) -> (status, objective, dual)`."""
+    if subgraph_cap <= 0:
+        milp = None
+    else:
+        if milp is ...:
+            milp = reference_milp_solver()
+        if milp is None:
+            raise ValueError(
+                f"lower_bound: subgraph_cap={subgraph_cap} needs an exact "
+                "sub-solver for subgraphs of at most that many tasks; pass "
+                "milp=... (e.g. bounds.reference_milp_solver() with the "
+                "reference installed) or subgraph_cap=0 for critical paths")
+    vals = _SubgraphValues(g, hw, table, timeout, subgraph_cap, milp, workers)
     modules = decomposition.modules
     T = len(modules)
     terms: list[dict] = []

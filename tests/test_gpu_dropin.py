@@ -1,0 +1,150 @@
+"""The drop-in, executed: the REFERENCE's own drivers (hetsched, imported
+unmodified from oracle/_ref or /root/reference through oracle/ref.py) run
+with their call-time globals re-bound to the B200 path by
+``integrate.patch_reference()``, and compared with
+
+* the reference's own results frozen in tests/golden (search_big.json:
+  SA / (1+1) EA at budget 2000, seeds 0-2 on WS 10x20, WS200 and the 96-layer
+  transformer; heuristics.json: best_device / met; bounds_cap40.json:
+  lower_bound at its default subgraph cap of 40, MILP terms included);
+* this package's own device-resident runs of the same drivers;
+* the reference's milp_split driving ``gpu_module_solver`` from 8 threads,
+  whose schedule must pass the reference's validate_schedule and equal this
+  package's milp_split with the same solver.
+"""
+from __future__ import annotations
+
+import json
+import sys
+
+import pytest
+
+from conftest import fhex, golden, instance_doc
+
+import paper_2308_00127_b200 as hs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle import ref as R
+    if R.import_reference() is None:
+        pytest.skip("reference not importable")
+    from paper_2308_00127_b200.integrate import patch_reference
+    restore = patch_reference()
+    yield {"core": sys.modules["hetsched.core"],
+           "heur": sys.modules["hetsched.heuristics"],
+           "bounds": sys.modules["hetsched.bounds"],
+           "split": sys.modules["hetsched.splitting"]}
+    restore()
+
+
+def _ref_inst(ref, doc):
+    RC = ref["core"]
+    return (RC.load_graph(json.dumps(doc["graph"])),
+            RC.load_hardware(json.dumps(doc["hardware"])),
+            RC.load_latency(json.dumps(doc["latency"])))
+
+
+def _mapping(s):
+    return {b.task: b.device for b in s.batches}
+
+
+@pytest.mark.parametrize("name", ["ws_stack_10x20", "ws200", "tf96"])
+def test_patched_reference_search_north_star_scale(ref, name):
+    RH = ref["heur"]
+    assert RH.fitness.__module__ != "hetsched.heuristics"  # patched
+    rg, rhw, rt = _ref_inst(ref, instance_doc(name))
+    g, hw, t = hs.load_instance(instance_doc(name))
+    runs = [e for e in golden("search_big") if e["instance"] == name]
+    assert len(runs) == 6
+    for e in runs:
+        fn = RH.simulated_annealing if e["algo"] == "sa" else \
+            RH.one_plus_one_ea
+        s = fn(rg, rhw, rt, 1, seed=e["seed"], budget=e["budget"])
+        assert fhex(s.objective) == e["objective"], e
+        assert _mapping(s) == e["mapping"]
+        # and this package's device-resident search kernels (K10 / K9)
+        mine = (hs.simulated_annealing if e["algo"] == "sa" else
+                hs.one_plus_one_ea)(g, hw, t, 1, seed=e["seed"],
+                                    budget=e["budget"])
+        assert fhex(mine.objective) == e["objective"]
+        assert _mapping(mine) == e["mapping"]
+
+
+def test_patched_reference_constructive(ref):
+    RH = ref["heur"]
+    for e in golden("heuristics"):
+        rg, rhw, rt = _ref_inst(ref, e)
+        for label, fn in (("best_device", RH.best_device), ("met", RH.met)):
+            want = e[label]
+            if "error" in want:
+                with pytest.raises(ref["core"].ScheduleError):
+                    fn(rg, rhw, rt, e["L"])
+                continue
+            s = fn(rg, rhw, rt, e["L"])
+            assert fhex(s.objective) == want["objective"], (e["name"], label)
+            assert _mapping(s) == want["mapping"]
+
+
+def _cap40():
+    try:
+        return golden("bounds_cap40")
+    except FileNotFoundError:  # pragma: no cover - fixture not generated
+        return []
+
+
+@pytest.mark.parametrize("e", _cap40(),
+                         ids=lambda e: f"{e['instance']}_L{e['L']}")
+def test_lower_bound_default_cap(ref, e):
+    """cap = 40: the reference's lower_bound on the B200 building blocks
+    (patched) and this package's lower_bound with the reference MILP as its
+    explicit sub-solver, run 8 sub-solves at a time -- both equal the
+    reference's unpatched result."""
+    from paper_2308_00127_b200.bounds import reference_milp_solver
+    rg, rhw, rt = _ref_inst(ref, instance_doc(e["instance"]))
+    rd = ref["split"].k_edge_components(rg, 1)
+    rep = ref["bounds"].lower_bound(rg, rhw, rt, e["L"], rd, workers=8)
+    assert fhex(rep.lower_bound_ms) == e["lower_bound_ms"]
+    assert json.loads(json.dumps(rep.terms)) == e["terms"]
+    g, hw, t = hs.load_instance(instance_doc(e["instance"]))
+    mine = hs.lower_bound(g, hw, t, e["L"], hs.k_edge_components(g, 1),
+                          workers=8, milp=reference_milp_solver())
+    assert fhex(mine.lower_bound_ms) == e["lower_bound_ms"]
+    assert fhex(mine.throughput_upper_bound) == e["throughput_upper_bound"]
+    assert json.loads(json.dumps(mine.terms)) == e["terms"]
+
+
+def test_lower_bound_needs_a_subsolver():
+    g, hw, t = hs.load_instance(instance_doc("er_stack_10x10"))
+    d = hs.k_edge_components(g, 1)
+    with pytest.raises(ValueError):
+        hs.lower_bound(g, hw, t, 1, d, milp=None)
+
+
+@pytest.mark.parametrize("name", ["ws_stack_10x20", "er_stack_4x10_c2"])
+def test_reference_milp_split_with_gpu_module_solver(ref, name):
+    """splitting.py:259-402 (the reference's DP) calling the GPU module
+    solver from 8 threads; the result validates under the reference's own
+    validate_schedule and equals this package's DP (single-threaded) with
+    the same solver."""
+    RS, RC = ref["split"], ref["core"]
+    rg, rhw, rt = _ref_inst(ref, instance_doc(name))
+    solver = hs.gpu_module_solver()
+    want = RS.milp_split(rg, rhw, rt, 1, RS.k_edge_components(rg, 1),
+                         module_solver=solver, workers=8)
+    mk = RC.validate_schedule(rg, rhw, rt, RC.Schedule(
+        batches=tuple(RC.ScheduledBatch(task=b.task, device=b.device,
+                                        size=b.size, inputs=b.inputs,
+                                        start=b.start) for b in want.batches),
+        objective=want.objective, input_count=1))
+    assert mk == pytest.approx(want.objective, abs=1e-6)
+    g, hw, t = hs.load_instance(instance_doc(name))
+    got = hs.milp_split(g, hw, t, 1, hs.k_edge_components(g, 1),
+                        module_solver=solver, workers=1)
+    assert fhex(got.objective) == fhex(want.objective)
+    assert tuple(got.flags) == tuple(want.flags)
+    assert [(b.task, b.device, fhex(b.start)) for b in got.batches] == \
+        [(b.task, b.device, fhex(b.start)) for b in want.batches]
+    assert hs.validate_schedule(g, hw, t, got) == mk
