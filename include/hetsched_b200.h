@@ -206,6 +206,21 @@ int hs_ea_run_chunk(const hs_plan *plan, uint8_t *d_parent, double *d_fit,
                     int32_t n_children, int32_t first_child, int32_t *d_info,
                     void *stream);
 
+/* The EA's mutation stream on the device (K12), for `chains` independent
+ * numpy PCG64 generators: chain c starts at d_rng + 4c = {state lo, state
+ * hi, inc lo, inc hi} with d_buf + 2c = {has_uint32, uinteger} and draws,
+ * for each of `budget` children and each of n_tasks positions, random() <
+ * p and on a hit integers(n_dev) (heuristics.py:318-325). Output as CSR
+ * for hs_ea_run_multi: d_moff + c * (budget + 1) (absolute offsets), the
+ * mutated positions / values at d_mpos / d_mval + c * cap_per_chain.
+ * d_status[c] = 0 ok, 1 more than cap_per_chain mutations, 2 Lemire's
+ * rejection branch was reached (probability < n_dev / 2^32): the caller
+ * redraws such a chain on the host. The generators are not advanced. */
+int hs_ea_draw(int32_t chains, const uint64_t *d_rng, const uint32_t *d_buf,
+               int32_t n_tasks, int32_t n_dev, double p, int32_t budget,
+               int32_t *d_moff, int32_t *d_mpos, uint8_t *d_mval,
+               int64_t cap_per_chain, int32_t *d_status, void *stream);
+
 /* Simulated annealing (heuristics.py:259-299) in one launch, resumable.
  * All state lives in device buffers (in/out): d_genes [V] current genome,
  * d_best [V] best-ever genome, d_rng = numpy PCG64 {state lo, state hi,
@@ -219,6 +234,26 @@ int hs_ea_run_chunk(const hs_plan *plan, uint8_t *d_parent, double *d_fit,
 int hs_sa_run(const hs_plan *plan, uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng,
               uint32_t *d_buf, double *d_f, int32_t *d_istate, double alpha,
               int32_t n_dev, int32_t budget, int32_t window, void *stream);
+
+/* Independent annealing chains in one launch, one CTA (one SM) each -- e.g.
+ * the reference's simulated_annealing at `chains` seeds at once. Chain c's
+ * state sits at d_genes / d_best + c * chain_stride (chain_stride >= V),
+ * d_rng + 4c, d_buf + 2c, d_f + 8c, d_istate + 8c, each laid out as in
+ * hs_sa_run; every chain follows its own seed's reference trajectory. */
+int hs_sa_run_multi(const hs_plan *plan, int32_t chains, int64_t chain_stride,
+                    uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng, uint32_t *d_buf,
+                    double *d_f, int32_t *d_istate, double alpha, int32_t n_dev,
+                    int32_t budget, int32_t window, void *stream);
+
+/* Independent (1+1) EA accept chains in one launch, one CTA each: chain c's
+ * parent at d_parent + c * chain_stride with fitness d_cur_fit[c], its
+ * mutation lists as CSR with offsets d_moff + c * (budget + 1) (absolute
+ * indices into d_mpos / d_mval), result d_fit[c] and d_info + 4c as in
+ * hs_ea_run. */
+int hs_ea_run_multi(const hs_plan *plan, int32_t chains, int64_t chain_stride,
+                    uint8_t *d_parent, const double *d_cur_fit, const int32_t *d_moff,
+                    const int32_t *d_mpos, const uint8_t *d_mval, int32_t budget,
+                    double *d_fit, int32_t *d_info, void *stream);
 
 /* On-device candidates: candidate c in [first, first+n) has genes
  * oracle/hs_oracle.py::gen_genes(seed, c). Optional d_genes_out [n x V]. */

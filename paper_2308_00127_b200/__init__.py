@@ -18,6 +18,7 @@ from .heuristics import (MappingGenome, argmin_batch, best_device, decode,
                          fitness, fitness_batch, fitness_batch_packed,
                          genome_from_map, greedy, met, pack_genes, pack_genes3,
                          one_plus_one_ea, random_search, simulated_annealing,
+                         simulated_annealing_multi, one_plus_one_ea_multi,
                          specialize, throughput)
 from .bounds import (BoundReport, critical_path_bound, critical_path_bounds,
                      dep_subgraph, lower_bound, pre_subgraph)

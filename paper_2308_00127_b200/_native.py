@@ -104,6 +104,12 @@ def load() -> C.CDLL:
                                           vp, vp]),
             "hs_sa_run": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_double,
                                     i32, i32, i32, vp]),
+            "hs_sa_run_multi": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp,
+                                          vp, C.c_double, i32, i32, i32, vp]),
+            "hs_ea_run_multi": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp,
+                                          i32, vp, vp, vp]),
+            "hs_ea_draw": (C.c_int, [i32, vp, vp, i32, i32, C.c_double, i32,
+                                     vp, vp, vp, i64, vp, vp]),
             "hs_eval_gen": (C.c_int, [vp, C.c_uint64, i64, i64, vp, vp, vp,
                                       vp, vp]),
             "hs_eval_gen_ex": (C.c_int, [vp, C.c_int, C.c_uint64, i64, i64,
@@ -141,7 +147,8 @@ def exported_symbols() -> list[str]:
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_packed", "hs_eval_host_packed",
             "hs_eval_packed3", "hs_eval_host_packed3", "hs_ea_run",
-            "hs_ea_run_chunk", "hs_sa_run", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
+            "hs_ea_run_chunk", "hs_sa_run", "hs_sa_run_multi",
+            "hs_ea_run_multi", "hs_ea_draw", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",
             "hs_cp_bound", "hs_reach", "hs_modularity", "hs_best_merge",
             "hs_best_allreduce", "hs_bridges_articulation",
             "hs_k_edge_components", "hs_validate_schedules"]

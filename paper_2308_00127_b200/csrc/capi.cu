@@ -348,7 +348,8 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
 // K9 / K10 setup: the evaluator parameters of one CTA of ds->T lanes (AOT
 // body); `ends_g` receives the global slot tier's scratch when needed.
 int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalParams &a,
-                      Scratch &ends_g, cudaStream_t stream, const hs::JitModule **jmp) {
+                      Scratch &ends_g, cudaStream_t stream, const hs::JitModule **jmp,
+                      int chains = 1) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
     const hs::Plan &p = plan->p;
     if (p.batched) return set_err(HS_EINVAL, "the search kernels run on non-batched plans");
@@ -393,7 +394,7 @@ int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalPar
     ends_g.s = stream;
     if (jm ? jm->ends_global : ds->ends_global) {
         a.ends_g_cta = int64_t(a.slots) * a.lanes;
-        CK(cudaMallocAsync(&ends_g.ptr, size_t(a.ends_g_cta) * 8, stream));
+        CK(cudaMallocAsync(&ends_g.ptr, size_t(a.ends_g_cta) * 8 * size_t(chains), stream));
         a.ends_g = static_cast<double *>(ends_g.ptr);
     }
     return HS_OK;
@@ -402,17 +403,20 @@ int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalPar
 int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *moff,
            const int32_t *mpos, const uint8_t *mval, int32_t budget, double *out_fit,
            int32_t *info, cudaStream_t stream, const double *cur_in = nullptr,
-           int32_t first_child = -1) {
+           int32_t first_child = -1, int32_t chains = 1, int64_t chain_stride = 0) {
     if (budget < 0 || !parent || !out_fit || !info || (budget > 0 && !moff))
         return set_err(HS_EINVAL, "bad EA arguments");
     const hs::DevState *ds = nullptr;
     const hs::JitModule *jm = nullptr;
     hs::EvalParams a{};
     Scratch ends_g;
-    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm);
+    if (chains < 1 || (chains > 1 && chain_stride < plan->p.V))
+        return set_err(HS_EINVAL, "bad EA chain count / stride");
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm, chains);
     if (rc) return rc;
     std::string err;
     hs::EaParams e{};
+    e.chain_stride = chains > 1 ? chain_stride : 0;
     e.parent = parent;
     e.cur_fit = cur_fit;
     e.moff = moff;
@@ -426,16 +430,17 @@ int run_ea(const hs_plan *plan, uint8_t *parent, double cur_fit, const int32_t *
     e.cur_in = cur_in;
     e.first_child = first_child;
     e.accumulate = first_child >= 0;
-    if (!e.accumulate) CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t), stream));
-    rc = jm ? hs::jit_launch_search(*jm, 2, a, &e, stream, &err)
-            : hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    if (!e.accumulate) CK(cudaMemsetAsync(info, 0, 4 * sizeof(int32_t) * size_t(chains), stream));
+    rc = jm ? hs::jit_launch_search(*jm, 2, a, &e, stream, &err, chains)
+            : hs::launch_ea(*ds, !plan->p.uniform_comm, a, e, stream, &err, chains);
     if (rc) return set_err(rc, err);
     return HS_OK;
 }
 
 int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
            uint32_t *buf, double *f, int32_t *istate, double alpha, int32_t n_dev,
-           int32_t budget, int32_t window, cudaStream_t stream) {
+           int32_t budget, int32_t window, cudaStream_t stream, int32_t chains = 1,
+           int64_t chain_stride = 0) {
     if (!genes || !best || !rng || !buf || !f || !istate || n_dev < 1 || n_dev > 256 ||
         budget < 0 || window < 1)
         return set_err(HS_EINVAL, "bad SA arguments");
@@ -443,7 +448,9 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     const hs::JitModule *jm = nullptr;
     hs::EvalParams a{};
     Scratch ends_g;
-    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm);
+    if (chains < 1 || (chains > 1 && chain_stride < plan->p.V))
+        return set_err(HS_EINVAL, "bad SA chain count / stride");
+    int rc = single_cta_params(plan, &ds, a, ends_g, stream, &jm, chains);
     if (rc) return rc;
     if (n_dev != plan->p.K) return set_err(HS_EINVAL, "n_dev != number of devices");
     std::string err;
@@ -451,12 +458,16 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.window = std::min(window, a.lanes);
     Scratch spec;
     spec.s = stream;
-    CK(cudaMallocAsync(&spec.ptr, size_t(e.window) * 16 + 64, stream));
+    // speculation scratch, one window per chain: [fit f64 | pos i32 | new
+    // u8 | status u8] x (chains * window)
+    const size_t nw = size_t(e.window) * size_t(chains);
+    CK(cudaMallocAsync(&spec.ptr, nw * 16 + 64, stream));
     uint8_t *sp = static_cast<uint8_t *>(spec.ptr);
     e.sfit = reinterpret_cast<double *>(sp);
-    e.spos = reinterpret_cast<int32_t *>(sp + size_t(e.window) * 8);
-    e.snew = sp + size_t(e.window) * 12;
-    e.sst = sp + size_t(e.window) * 13;
+    e.spos = reinterpret_cast<int32_t *>(sp + nw * 8);
+    e.snew = sp + nw * 12;
+    e.sst = sp + nw * 13;
+    e.chain_stride = chains > 1 ? chain_stride : 0;
     e.genes = genes;
     e.best = best;
     e.rng = reinterpret_cast<hs_u64 *>(rng);
@@ -468,8 +479,8 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.budget = budget;
     const char *hx = getenv("HS_SA_HOST_EXP");
     e.host_exp = hx && atoi(hx) ? 1 : 0;
-    rc = jm ? hs::jit_launch_search(*jm, 1, a, &e, stream, &err)
-            : hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err);
+    rc = jm ? hs::jit_launch_search(*jm, 1, a, &e, stream, &err, chains)
+            : hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err, chains);
     if (rc) return set_err(rc, err);
     return HS_OK;
 }
@@ -865,6 +876,23 @@ int hs_sa_run(const hs_plan *plan, uint8_t *d_genes, uint8_t *d_best, uint64_t *
               int32_t n_dev, int32_t budget, int32_t window, void *stream) {
     return run_sa(plan, d_genes, d_best, d_rng, d_buf, d_f, d_istate, alpha, n_dev, budget,
                   window, static_cast<cudaStream_t>(stream));
+}
+
+int hs_sa_run_multi(const hs_plan *plan, int32_t chains, int64_t chain_stride,
+                    uint8_t *d_genes, uint8_t *d_best, uint64_t *d_rng, uint32_t *d_buf,
+                    double *d_f, int32_t *d_istate, double alpha, int32_t n_dev,
+                    int32_t budget, int32_t window, void *stream) {
+    return run_sa(plan, d_genes, d_best, d_rng, d_buf, d_f, d_istate, alpha, n_dev, budget,
+                  window, static_cast<cudaStream_t>(stream), chains, chain_stride);
+}
+
+int hs_ea_run_multi(const hs_plan *plan, int32_t chains, int64_t chain_stride,
+                    uint8_t *d_parent, const double *d_cur_fit, const int32_t *d_moff,
+                    const int32_t *d_mpos, const uint8_t *d_mval, int32_t budget,
+                    double *d_fit, int32_t *d_info, void *stream) {
+    if (!d_cur_fit) return set_err(HS_EINVAL, "null start fitness");
+    return run_ea(plan, d_parent, 0.0, d_moff, d_mpos, d_mval, budget, d_fit, d_info,
+                  static_cast<cudaStream_t>(stream), d_cur_fit, -1, chains, chain_stride);
 }
 
 int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,

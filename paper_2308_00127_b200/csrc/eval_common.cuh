@@ -119,6 +119,11 @@ struct EaParams {
     int first_child, accumulate;
     double *out_fit;      // [1] final fitness
     int *info;            // [4] accepted, rounds, raising child (-1), status
+    // independent chains (hs_ea_run_multi): CTA c runs chain c with its
+    // parent at parent + c * chain_stride, its CSR offsets at moff + c *
+    // (budget + 1) (absolute indices into mpos / mval), out_fit + c and
+    // info + 4 c; 0 = one chain
+    hs_i64 chain_stride;
 };
 
 // simulated annealing (K10); all state in/out so a run can resume
@@ -138,6 +143,10 @@ struct SaParams {
     double alpha;
     int n_dev, budget, window;
     int host_exp;      // test hook: hand every Metropolis test to the host
+    // independent chains (hs_sa_run_multi): CTA c runs chain c with genes /
+    // best at + c * chain_stride, rng + 4c, buf + 2c, f + 8c, istate + 8c and
+    // its own speculation scratch (+ c * window); 0 = one chain
+    hs_i64 chain_stride;
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
@@ -146,7 +155,11 @@ __device__ __forceinline__ double kinf() { return __longlong_as_double(0x7ff0000
 __device__ __forceinline__ double knan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 __device__ __forceinline__ double pymax(double a, double b) {
-    return b > a ? b : a;  // Python max(a, b): a unless b > a
+    // Python max(a, b): a unless b > a (NaN compares false: a)
+    double r;
+    asm("{\n .reg .pred p;\n setp.gt.f64 p, %2, %1;\n selp.f64 %0, %2, %1, p;\n}"
+        : "=d"(r) : "d"(a), "d"(b));
+    return r;
 }
 
 // Tensor-memory tier of the specialised kernel's end-time slots: each
@@ -172,7 +185,12 @@ __device__ __forceinline__ double tm_val(hs_u32 lo, hs_u32 hi) {
 // (p && v > r) ? v : r -- one compare with a predicate input and a 64-bit
 // select (the specialised kernel's dominance-pruned relaxation term)
 __device__ __forceinline__ double maxsel(double r, bool p, double v) {
-    return (p & (v > r)) ? v : r;
+    // one compare with the predicate folded in (setp.gt.and) + one select
+    double out;
+    asm("{\n .reg .pred q, s;\n setp.ne.b32 q, %3, 0;\n"
+        " setp.gt.and.f64 s, %2, %1, q;\n selp.f64 %0, %2, %1, s;\n}"
+        : "=d"(out) : "d"(r), "d"(v), "r"((int)p));
+    return out;
 }
 
 // Python max(a, b) for a, b >= +0.0 and not NaN: the binary64 bit patterns
@@ -237,6 +255,9 @@ __device__ __forceinline__ hs_u32 smem_addr(const void *p) {
     return (hs_u32)__cvta_generic_to_shared(p);
 }
 
+__device__ __forceinline__ void mbar_inval(hs_u64 *bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_init(hs_u64 *bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -560,6 +581,13 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
             }
         }
     }
+    // the mbarriers' lifetime ends with the tile loop (no copy in flight):
+    // invalidate them before the shared memory is reused
+    __syncthreads();
+    if (tid == 0) {
+        mbar_inval(bar);
+        mbar_inval(bar + 1);
+    }
     if (a.best) reduce_best(bc, bi, a.partial, a.ticket, a.best);
 }
 
@@ -622,9 +650,23 @@ struct Pcg64 {
 // practice), so the trajectory is the reference's exactly. Shared by the
 // AOT kernel (kernels.cu) and the specialised module (jit.cpp).
 template <class Body>
-__device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e, hs_u8 *smem,
+__device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0, hs_u8 *smem,
                                          Body &body) {
     __shared__ int s_k, s_step, s_go, s_apos;
+    SaParams e = e0;  // this CTA's chain
+    if (e0.chain_stride) {
+        const hs_i64 c = blockIdx.x;
+        e.genes += c * e0.chain_stride;
+        e.best += c * e0.chain_stride;
+        e.rng += 4 * c;
+        e.buf += 2 * c;
+        e.f += 8 * c;
+        e.istate += 8 * c;
+        e.spos += c * e0.window;
+        e.snew += c * e0.window;
+        e.sfit += c * e0.window;
+        e.sst += c * e0.window;
+    }
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
     hs_u8 *genes = e.genes;
@@ -790,9 +832,18 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e,
 // a full round. Children after an acceptance are re-evaluated against the
 // new parent in the next round, so the trajectory is the reference's.
 template <class Body>
-__device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e, hs_u8 *smem,
+__device__ __forceinline__ void ea_chain(const EvalParams &a, const EaParams &e0, hs_u8 *smem,
                                          Body &body) {
     __shared__ int s_first, s_first2;
+    EaParams e = e0;  // this CTA's chain
+    if (e0.chain_stride) {
+        const hs_i64 c = blockIdx.x;
+        e.parent += c * e0.chain_stride;
+        e.moff += c * (hs_i64)(e0.budget + 1);
+        e.out_fit += c;
+        e.info += 4 * c;
+        if (e.cur_in) e.cur_in += c;
+    }
     __shared__ double s_fit, s_fit2;
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;

@@ -518,22 +518,34 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
             if (!in_reg) qs.push_back(q);
         }
         const std::string is = std::to_string(i);
+        // one asm block per group of <= 8: the loads into 32-bit temporaries,
+        // one wait, then each pair moved into a true 64-bit output (a double
+        // assembled from two separately-tied registers costs ptxas a
+        // register-pair copy before every 64-bit use)
         for (size_t c = 0; c < qs.size(); c += 8) {
-            std::string outs;
-            for (size_t k = c; k < std::min(qs.size(), c + 8); ++k) {
-                const std::string v = "TV" + is + "_" + std::to_string(qs[k]);
-                s += "    hs_u32 " + v + "l, " + v + "h;\n";
-                s += "    tm_ld2(TB + " + std::to_string(2 * where[qs[k]]) + ", " + v + "l, " + v +
-                     "h);\n";
-                outs += std::string(outs.empty() ? "" : ", ") + "\"+r\"(" + v + "l), \"+r\"(" + v +
-                        "h)";
+            const size_t m = std::min(qs.size(), c + 8) - c;
+            std::string body = "{\\n .reg .b32 ";
+            for (size_t k = 0; k < m; ++k)
+                body += (k ? ", " : "") + std::string("l") + std::to_string(k) + ", h" +
+                        std::to_string(k);
+            body += ";\\n";
+            for (size_t k = 0; k < m; ++k)
+                body += " tcgen05.ld.sync.aligned.32x32b.x2.b32 {l" + std::to_string(k) + ", h" +
+                        std::to_string(k) + "}, [%" + std::to_string(m + k) + "];\\n";
+            body += " tcgen05.wait::ld.sync.aligned;\\n";
+            for (size_t k = 0; k < m; ++k)
+                body += " mov.b64 %" + std::to_string(k) + ", {l" + std::to_string(k) + ", h" +
+                        std::to_string(k) + "};\\n";
+            body += "}";
+            std::string outs, ins;
+            for (size_t k = 0; k < m; ++k) {
+                const std::string v = "TV" + is + "_" + std::to_string(qs[c + k]);
+                s += "    double " + v + ";\n";
+                outs += std::string(k ? ", " : "") + "\"=d\"(" + v + ")";
+                ins += std::string(k ? ", " : "") + "\"r\"(TB + " +
+                       std::to_string(2 * where[qs[c + k]]) + "u)";
             }
-            s += "    asm volatile(\"tcgen05.wait::ld.sync.aligned;\" : " + outs +
-                 " :: \"memory\");\n";
-            for (size_t k = c; k < std::min(qs.size(), c + 8); ++k) {
-                const std::string v = "TV" + is + "_" + std::to_string(qs[k]);
-                s += "    const double " + v + " = tm_val(" + v + "l, " + v + "h);\n";
-            }
+            s += "    asm volatile(\"" + body + "\" : " + outs + " : " + ins + " : \"memory\");\n";
         }
     };
     auto head = [&](int i) {
@@ -638,8 +650,15 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         std::string stored = ei;
         if (dom && last[i] >= 0) {
             stored = "f" + is;
-            s += "    const double " + stored + " = " +
-                 (zero_c(i) ? ei : ei + " + " + lit(prod_c[i])) + ";\n";
+            // the constant from constant memory: a DADD operand (c[3][..]),
+            // where an immediate double costs two UMOVs per task
+            std::string cv = lit(prod_c[i]);
+            if (!zero_c(i) && std::isfinite(prod_c[i])) {
+                cv = "HSC[" + std::to_string(cconst.size()) + "]";
+                cconst.push_back(prod_c[i]);
+            }
+            s += "    const double " + stored + " = " + (zero_c(i) ? ei : ei + " + " + cv) +
+                 ";\n";
         }
         if (where[i] >= 0) {
             if (o.tmem)
@@ -966,6 +985,21 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     std::vector<char> cubin(csz);
     nv.cubin(prog, cubin.data());
     nv.destroy(&prog);
+    // HS_JIT_DUMP=<dir>: keep the emitted source and cubin (cuobjdump -sass
+    // for the SASS listings under profiles/)
+    if (const char *dir = getenv("HS_JIT_DUMP")) {
+        char stem[512];
+        std::snprintf(stem, sizeof stem, "%s/hs_jit_V%d_E%d_K%d_L%d_T%d", dir, p.V, p.E,
+                      p.K, p.L, T);
+        if (FILE *f = std::fopen((std::string(stem) + ".cu").c_str(), "wb")) {
+            std::fwrite(src.data(), 1, src.size(), f);
+            std::fclose(f);
+        }
+        if (FILE *f = std::fopen((std::string(stem) + ".cubin").c_str(), "wb")) {
+            std::fwrite(cubin.data(), 1, cubin.size(), f);
+            std::fclose(f);
+        }
+    }
 
     JitModule *m = new JitModule();
     m->device = device;
@@ -1047,14 +1081,14 @@ bool jit_direct_ok(const JitModule &m, const hsk::EvalParams &a) {
 }
 
 int jit_launch_search(const JitModule &m, int mode, const hsk::EvalParams &a,
-                      const void *ps, cudaStream_t stream, std::string *err) {
+                      const void *ps, cudaStream_t stream, std::string *err, int grid) {
     const cudaKernel_t k = mode == 1 ? m.kern_sa : m.kern_ea;
     if (!k) {
         if (err) *err = "specialised module has no search kernels";
         return HS_EINVAL;
     }
     void *args[] = {(void *)&a, const_cast<void *>(ps)};
-    cudaError_t e = cudaLaunchKernel((const void *)k, dim3(1), dim3(m.T), args, m.smem, stream);
+    cudaError_t e = cudaLaunchKernel((const void *)k, dim3(grid), dim3(m.T), args, m.smem, stream);
     if (e != cudaSuccess) {
         if (err) *err = std::string("specialised search launch: ") + cudaGetErrorString(e);
         return HS_ECUDA;

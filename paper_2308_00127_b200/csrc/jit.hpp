@@ -70,6 +70,6 @@ int jit_launch(const JitModule &m, const hsk::EvalParams &a, int grid,
                cudaStream_t stream, std::string *err);
 // one CTA of the SA (mode 1) or EA (mode 2) search kernel; `ps` -> params
 int jit_launch_search(const JitModule &m, int mode, const hsk::EvalParams &a,
-                      const void *ps, cudaStream_t stream, std::string *err);
+                      const void *ps, cudaStream_t stream, std::string *err, int grid = 1);
 
 }  // namespace hs

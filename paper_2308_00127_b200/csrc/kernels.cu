@@ -337,7 +337,10 @@ __device__ __forceinline__ void single_cta_body(const EvalParams &a, hs_u8 *smem
     body.bclass = reinterpret_cast<const hs_u16 *>(plan + a.lay.bclass);
     body.cap = reinterpret_cast<const double *>(plan + a.lay.cap);
     body.okL = plan + a.lay.okL;
-    body.ends = a.ends_g ? a.ends_g : reinterpret_cast<double *>(smem + a.smem_ends);
+    // one CTA per chain (hs_sa_run_multi / hs_ea_run_multi): each its own
+    // region of the global slot tier
+    body.ends = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta
+                         : reinterpret_cast<double *>(smem + a.smem_ends);
     body.kstate = reinterpret_cast<double *>(smem + a.smem_kstate);
     body.starts = nullptr;
     body.lanes = a.lanes;
@@ -611,13 +614,13 @@ static void *pick_ea(int kt, bool cls, bool fast) {
 }
 
 int launch_ea(const DevState &ds, bool cls, const EvalParams &p, const EaParams &ea,
-              cudaStream_t stream, std::string *err) {
+              cudaStream_t stream, std::string *err, int grid) {
     void *fn = pick_ea(ds.kt, cls, p.flags == 0);
     cudaError_t e = cudaFuncSetAttribute(
         fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ds.smem);
     if (e != cudaSuccess) return cuda_fail(e, err, "cudaFuncSetAttribute");
     void *args[] = {(void *)&p, (void *)&ea};
-    e = cudaLaunchKernel(fn, dim3(1), dim3(ds.T), args, ds.smem, stream);
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(ds.T), args, ds.smem, stream);
     if (e != cudaSuccess) return cuda_fail(e, err, "ea launch");
     return HS_OK;
 }
@@ -637,13 +640,13 @@ static void *pick_sa(int kt, bool cls, bool fast) {
 }
 
 int launch_sa(const DevState &ds, bool cls, const EvalParams &p, const SaParams &sa,
-              cudaStream_t stream, std::string *err) {
+              cudaStream_t stream, std::string *err, int grid) {
     void *fn = pick_sa(ds.kt, cls, p.flags == 0);
     cudaError_t e = cudaFuncSetAttribute(
         fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ds.smem);
     if (e != cudaSuccess) return cuda_fail(e, err, "cudaFuncSetAttribute");
     void *args[] = {(void *)&p, (void *)&sa};
-    e = cudaLaunchKernel(fn, dim3(1), dim3(ds.T), args, ds.smem, stream);
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(ds.T), args, ds.smem, stream);
     if (e != cudaSuccess) return cuda_fail(e, err, "sa launch");
     return HS_OK;
 }

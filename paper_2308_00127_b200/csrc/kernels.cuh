@@ -25,10 +25,11 @@ int launch_beval(const DevState &ds, const EvalParams &p, int grid,
                  cudaStream_t stream, std::string *err);
 int launch_eval(const DevState &ds, bool cls, const EvalParams &p, int grid,
                 cudaStream_t stream, std::string *err);
+// grid = number of independent chains (one CTA each)
 int launch_sa(const DevState &ds, bool cls, const EvalParams &p, const SaParams &sa,
-              cudaStream_t stream, std::string *err);
+              cudaStream_t stream, std::string *err, int grid = 1);
 int launch_ea(const DevState &ds, bool cls, const EvalParams &p, const EaParams &ea,
-              cudaStream_t stream, std::string *err);
+              cudaStream_t stream, std::string *err, int grid = 1);
 int launch_cp(const uint8_t *blob, const DevLayout &lay, int V, int words,
               const uint64_t *masks, int64_t nsub, double *out, uint8_t *status,
               double *scratch, cudaStream_t stream, std::string *err);

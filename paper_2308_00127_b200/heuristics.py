@@ -681,6 +681,98 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     return out
 
 
+def _pcg_words(seed: int):
+    """(PCG64 state words [4], buffered uint32 [2]) of default_rng(seed)."""
+    bs = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(bs["state"]["state"]), int(bs["state"]["inc"])
+    return ([s & _M64, s >> 64, inc & _M64, inc >> 64],
+            [bs["has_uint32"], bs["uinteger"]])
+
+
+def _decode_rows(plan: Plan, g, hw, table, L: int, rows: np.ndarray) -> list:
+    """Schedules of many genomes in one trace launch (as decode())."""
+    ms, st, starts = _eval_rows(plan, rows, trace=True)
+    devs = sorted(hw.devices)
+    inputs = tuple(range(1, L + 1))
+    out = []
+    for r in range(len(rows)):
+        _raise_status(int(st[r]))
+        if int(st[r]) != N.ST_OK:
+            out.append(None)
+            continue
+        out.append(Schedule(batches=tuple(
+            ScheduledBatch(task=t, device=devs[int(rows[r, i])], size=L,
+                           inputs=inputs, start=float(starts[r, i]))
+            for i, t in enumerate(plan.order)), objective=float(ms[r]),
+            input_count=L))
+    return out
+
+
+@_gc_paused
+def simulated_annealing_multi(g, hw, table, L: int, seeds: Sequence[int],
+                              budget: int = 2000, t0_fraction: float = 0.1,
+                              alpha: float = 0.995,
+                              window: int = 128) -> list:
+    """simulated_annealing at every seed of `seeds` at once: one K10 chain
+    per seed, one CTA (one SM) each, all in one launch (hs_sa_run_multi), so
+    148 independent restarts take about one run's time on a B200. Element c
+    is exactly ``simulated_annealing(g, hw, table, L, seed=seeds[c],
+    budget=budget, ...)`` (each chain replays its own seed's PCG64 stream);
+    a chain that needs the host -- a Metropolis test within a few ulp of the
+    device exp, or an evaluation that raises -- is finished by the
+    single-chain path. Returns the Schedules in seed order; the best restart
+    is ``min(result, key=lambda s: s.objective)``."""
+    import torch
+    seeds = [int(s) for s in seeds]
+    if not seeds:
+        return []
+    start = greedy(g, hw, table, L)
+    cur = genome_from_map(g, hw, {b.task: b.device for b in start.batches})
+    cur_fit = fitness(cur, g, hw, table, L)
+    V = len(cur.genes)
+    if V == 0 or budget <= 0:
+        return [simulated_annealing(g, hw, table, L, seed=s, budget=budget,
+                                    t0_fraction=t0_fraction, alpha=alpha)
+                for s in seeds]
+    temp = max(t0_fraction * cur_fit, 1e-9)
+    n_dev = len(hw.devices)
+    plan = get_plan(g, hw, table, L)
+    C = len(seeds)
+    stride = -(-V // 16) * 16
+    rows = np.zeros((C, stride), np.uint8)
+    rows[:, :V] = np.asarray(cur.genes, np.uint8)
+    rng = np.zeros((C, 4), np.uint64)
+    buf = np.zeros((C, 2), np.uint32)
+    for c, s in enumerate(seeds):
+        w, b = _pcg_words(s)
+        rng[c] = w
+        buf[c] = b
+    f = np.zeros((C, 8), np.float64)
+    f[:, 0] = f[:, 1] = cur_fit
+    f[:, 2] = temp
+    ist = np.zeros((C, 8), np.int32)
+    ist[:, 1] = 8
+    dev = torch.device("cuda")
+    d_genes = torch.from_numpy(rows).to(dev)
+    d_best = d_genes.clone()
+    d_rng = torch.from_numpy(rng.view(np.int64)).to(dev)
+    d_buf = torch.from_numpy(buf.view(np.int32)).to(dev)
+    d_f = torch.from_numpy(f).to(dev)
+    d_ist = torch.from_numpy(ist).to(dev)
+    plan.sa_run_multi(C, d_genes, d_best, d_rng, d_buf, d_f, d_ist, alpha,
+                      n_dev, budget, max(window, 128))
+    iv = d_ist.cpu().numpy()
+    best = np.ascontiguousarray(d_best.cpu().numpy()[:, :V])
+    _last_chain_stats["sa_multi_rounds"] = [int(x) for x in iv[:, 6]]
+    out = _decode_rows(plan, g, hw, table, L, best)
+    for c in range(C):
+        if iv[c, 2] != 0 or out[c] is None:
+            out[c] = simulated_annealing(g, hw, table, L, seed=seeds[c],
+                                         budget=budget,
+                                         t0_fraction=t0_fraction, alpha=alpha)
+    return out
+
+
 def _ea_draw_chunk(gen, steps: int, V: int, n_dev: int, p: float):
     """Mutation lists of the next `steps` EA children as CSR arrays in
     pinned host memory; moves `gen` past them."""
@@ -710,15 +802,67 @@ def _ea_draw_chunk(gen, steps: int, V: int, n_dev: int, p: float):
     return moff, mpos[:len(flat)], mval[:len(flat)]
 
 
+def _ea_draw_device(states, V: int, n_dev: int, p: float, budget: int):
+    """K12 (hs_ea_draw): the mutation lists of `budget` EA children for
+    every generator state in `states` [(words[4], buf[2])], drawn on the
+    device. Returns (moff [C, budget+1] absolute, mpos, mval, status [C])
+    as device tensors; status != 0 marks a chain the host must redraw."""
+    import torch
+    from . import _native as NN
+    C = len(states)
+    dev = torch.device("cuda")
+    rng = torch.from_numpy(np.array([w for w, _ in states], np.uint64)
+                           .view(np.int64)).to(dev)
+    buf = torch.from_numpy(np.array([b for _, b in states], np.uint32)
+                           .view(np.int32)).to(dev)
+    cap = 4 * budget + 256
+    moff = torch.empty((C, budget + 1), dtype=torch.int32, device=dev)
+    mpos = torch.empty(C * cap, dtype=torch.int32, device=dev)
+    mval = torch.empty(C * cap, dtype=torch.uint8, device=dev)
+    status = torch.empty(C, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream()
+    NN.check(NN.load().hs_ea_draw(
+        C, rng.data_ptr(), buf.data_ptr(), V, n_dev, float(p), budget,
+        moff.data_ptr(), mpos.data_ptr(), mval.data_ptr(), cap,
+        status.data_ptr(), int(s.cuda_stream)), "hs_ea_draw")
+    return moff, mpos, mval, status, (rng, buf)
+
+
+def _gen_words(gen):
+    bs = gen.bit_generator.state
+    s, inc = int(bs["state"]["state"]), int(bs["state"]["inc"])
+    return ([s & _M64, s >> 64, inc & _M64, inc >> 64],
+            [bs["has_uint32"], bs["uinteger"]])
+
+
 def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
                      budget: int, V: int, n_dev: int, p: float,
                      chunks: int = 4):
-    """The accept chain on the device (K9) in `chunks` chained launches
-    (hs_ea_run_chunk): the host draws chunk c+1's mutations while chunk c
-    runs. Returns (genes, fitness)."""
+    """The accept chain on the device (K9). The mutation lists come from
+    the device draw (K12) when it succeeds; otherwise the host draws them
+    in `chunks` chained launches (hs_ea_run_chunk), chunk c+1's draw
+    overlapping chunk c's run. Returns (genes, fitness)."""
     import torch
     dev = torch.device("cuda")
     stream = torch.cuda.current_stream()
+    moff, mpos, mval, status, keep_d = _ea_draw_device(
+        [_gen_words(gen)], V, n_dev, p, budget)
+    d_parent = torch.from_numpy(genes.copy()).to(dev)
+    d_cur = torch.tensor([cur_fit], dtype=torch.float64, device=dev)
+    d_fit = torch.empty(1, dtype=torch.float64, device=dev)
+    d_info = torch.empty(4, dtype=torch.int32, device=dev)
+    plan.ea_run_multi(1, d_parent.view(1, -1), d_cur, moff, mpos, mval,
+                      budget, d_fit, d_info, stream=stream)
+    if int(status.item()) == 0:
+        info = d_info.cpu().numpy()
+        _last_chain_stats["ea_accepted"] = int(info[0])
+        _last_chain_stats["ea_rounds"] = int(info[1])
+        _last_chain_stats["ea_draw"] = "device"
+        if info[2] >= 0:
+            _raise_status(int(info[3]))
+        return d_parent.cpu().numpy(), float(d_fit.cpu()[0])
+    del keep_d
+    _last_chain_stats["ea_draw"] = "host"
     d_parent = torch.from_numpy(genes.copy()).to(dev)
     d_fit = torch.tensor([cur_fit], dtype=torch.float64, device=dev)
     d_info = torch.tensor([0, 0, -1, 0], dtype=torch.int32, device=dev)
@@ -739,6 +883,65 @@ def _ea_device_chain(plan: Plan, gen, genes: np.ndarray, cur_fit: float,
     if info[2] >= 0:
         _raise_status(int(info[3]))
     return d_parent.cpu().numpy(), float(d_fit.cpu()[0])
+
+
+@_gc_paused
+def one_plus_one_ea_multi(g, hw, table, L: int, seeds: Sequence[int],
+                          budget: int = 2000, biased: bool = True) -> list:
+    """one_plus_one_ea at every seed of `seeds` at once: each seed's
+    mutation stream drawn on the device (K12), then one K9 accept chain per
+    seed, one CTA (one SM) each, in one launch (hs_ea_run_multi). Element c
+    is exactly ``one_plus_one_ea(g, hw, table, L, seed=seeds[c], budget=
+    budget, biased=biased)``; a chain whose draw needs the host, or whose
+    evaluation raises, is finished by the single-chain path."""
+    import torch
+    seeds = [int(s) for s in seeds]
+    if not seeds:
+        return []
+    order = tuple(bfs_topological_order(g))
+    n_dev = len(hw.devices)
+    V = len(order)
+    if V == 0 or budget <= 0:
+        return [one_plus_one_ea(g, hw, table, L, seed=s, budget=budget,
+                                biased=biased) for s in seeds]
+    plan = get_plan(g, hw, table, L)
+    C = len(seeds)
+    stride = -(-V // 16) * 16
+    rows = np.zeros((C, stride), np.uint8)
+    states = []
+    if biased:
+        start = genome_from_map(g, hw, {b.task: b.device for b in
+                                        met(g, hw, table, L).batches})
+        rows[:, :V] = np.asarray(start.genes, np.uint8)
+        fits = np.full(C, fitness(start, g, hw, table, L))
+        states = [_gen_words(np.random.default_rng(s)) for s in seeds]
+    else:
+        for c, s in enumerate(seeds):
+            gen = np.random.default_rng(s)
+            rows[c, :V] = gen.integers(n_dev, size=V)
+            states.append(_gen_words(gen))
+        fits = _fit_rows(plan, np.ascontiguousarray(rows[:, :V]))
+    p = 1.0 / max(V, 1)
+    moff, mpos, mval, status, keep_d = _ea_draw_device(states, V, n_dev, p,
+                                                       budget)
+    dev = torch.device("cuda")
+    d_parent = torch.from_numpy(rows).to(dev)
+    d_cur = torch.from_numpy(fits.astype(np.float64)).to(dev)
+    d_fit = torch.empty(C, dtype=torch.float64, device=dev)
+    d_info = torch.empty((C, 4), dtype=torch.int32, device=dev)
+    plan.ea_run_multi(C, d_parent, d_cur, moff, mpos, mval, budget, d_fit,
+                      d_info)
+    info = d_info.cpu().numpy()
+    st = status.cpu().numpy()
+    final = np.ascontiguousarray(d_parent.cpu().numpy()[:, :V])
+    del keep_d
+    _last_chain_stats["ea_multi_rounds"] = [int(x) for x in info[:, 1]]
+    out = _decode_rows(plan, g, hw, table, L, final)
+    for c in range(C):
+        if st[c] != 0 or info[c, 2] >= 0 or out[c] is None:
+            out[c] = one_plus_one_ea(g, hw, table, L, seed=seeds[c],
+                                     budget=budget, biased=biased)
+    return out
 
 
 @_gc_paused

@@ -310,6 +310,30 @@ class Plan:
             _ptr(f), _ptr(istate), float(alpha), int(n_dev), int(budget),
             int(window), self._stream(stream)), "hs_sa_run")
 
+    def sa_run_multi(self, chains: int, genes, best, rng, buf, f, istate,
+                     alpha: float, n_dev: int, budget: int, window: int,
+                     stream=None) -> None:
+        """hs_sa_run_multi: `chains` K10 chains, one CTA each; genes / best
+        uint8 [chains, stride], rng int64 [chains, 4], buf int32 [chains, 2],
+        f f64 [chains, 8], istate int32 [chains, 8] (contiguous)."""
+        N.check(self._lib.hs_sa_run_multi(
+            self.handle, int(chains), int(genes.stride(0)), _ptr(genes),
+            _ptr(best), _ptr(rng), _ptr(buf), _ptr(f), _ptr(istate),
+            float(alpha), int(n_dev), int(budget), int(window),
+            self._stream(stream)), "hs_sa_run_multi")
+
+    def ea_run_multi(self, chains: int, parent, cur_fit, moff, mpos, mval,
+                     budget: int, fit, info, stream=None) -> None:
+        """hs_ea_run_multi: `chains` K9 chains, one CTA each; parent uint8
+        [chains, stride] (in/out), cur_fit / fit f64 [chains], moff int32
+        [chains, budget + 1] (absolute), info int32 [chains, 4]."""
+        N.check(self._lib.hs_ea_run_multi(
+            self.handle, int(chains), int(parent.stride(0)), _ptr(parent),
+            _ptr(cur_fit), _ptr(moff),
+            _ptr(mpos) if mpos.numel() else None,
+            _ptr(mval) if mval.numel() else None, int(budget), _ptr(fit),
+            _ptr(info), self._stream(stream)), "hs_ea_run_multi")
+
     def packed3_ld(self) -> int:
         """Row bytes of base-3 packed genomes (5 genes per byte)."""
         return (self.V + 4) // 5

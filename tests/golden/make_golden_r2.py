@@ -310,17 +310,50 @@ def search_doc():
         return p.map(_search_job, jobs, chunksize=1)
 
 
+# ------------------------------------------------------- throughput mode
+def throughput_doc():
+    """test_acceptance.py:298-321: 20 random L=2 instances, the brute-force
+    optimum under the throughput objective (oracle.py:96-) and the batched
+    heuristics' schedules (which must never beat it)."""
+    from hetsched.core import save_hardware, save_latency
+    from hetsched.oracle import brute_force
+    random_instance = _ref_conftest().random_instance
+    out = []
+    L = 2
+    for seed in range(2000, 2020):
+        g, hw, t = random_instance(seed, max_tasks=5, max_devices=2, L=L,
+                                   allow_missing_links=False,
+                                   allow_tight_memory=False)
+        opt = brute_force(g, hw, t, L, objective="throughput")
+        e = {"seed": seed, "L": L, "graph": json.loads(save_graph(g)),
+             "hardware": json.loads(save_hardware(hw)),
+             "latency": json.loads(save_latency(t)),
+             "oracle_objective": fhex(opt.objective), "batched": {}}
+        for algo in ("met", "greedy", "heft"):
+            try:
+                s = batched_variant(algo, g, hw, t, L)
+            except ScheduleError:
+                continue
+            e["batched"][algo] = {"objective": fhex(s.objective),
+                                  **_sched_doc(s)}
+        out.append(e)
+    return out
+
+
 def main():
     # networkx's k-edge auxiliary graph recurses once per tree level
     # (RecursionError at the default limit on WS1000 with k >= 3)
     sys.setrecursionlimit(200000)
-    what = sys.argv[1:] or ["decomp", "validate", "bounds", "search"]
+    what = sys.argv[1:] or ["decomp", "validate", "search", "throughput",
+                            "bounds"]
     if "decomp" in what:
         dump("decomp.json", decomp_doc())
     if "validate" in what:
         dump("validate.json", validate_doc())
     if "search" in what:
         dump("search_big.json", search_doc())
+    if "throughput" in what:
+        dump("throughput.json", throughput_doc())
     if "bounds" in what:
         dump("bounds_cap40.json", bounds_doc())
 
