@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "host_pack.hpp"
 #include "jit.hpp"
 #include "kernels.cuh"
 #include "plan.hpp"
@@ -733,6 +734,117 @@ int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     return HS_OK;
 }
 
+// uint8 host genomes (the reference's layout), K <= 4: the host thread pool
+// packs each chunk to 2 bits per gene into a pinned staging buffer while
+// the GPU copies and evaluates the previous one (double-buffered), so the
+// PCIe link -- the bound of this path -- carries ceil(V/4) instead of V
+// bytes per candidate. A chunk holding a gene >= K goes over unpacked, so
+// the kernel flags it (status 5) exactly as on the unpacked path.
+int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, int64_t ld,
+                        double *h_makespan, uint8_t *h_status, hs_best *h_best,
+                        int64_t index_base, cudaStream_t s0) {
+    const hs::Plan &p = plan->p;
+    const int V = p.V;
+    const int64_t pld = ((V + 3) / 4 + 3) / 4 * 4;
+    const int64_t chunk = std::min<int64_t>(n, 1 << 19);
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const size_t gbytes = size_t(chunk) * size_t(std::max<int64_t>(ld, pld));
+    const size_t per = ((gbytes + 255) & ~size_t(255)) + size_t(chunk) * 8 +
+                       ((size_t(chunk) + 255) & ~size_t(255));
+    uint8_t *stage[2] = {hs::pinned_staging(0, size_t(chunk * pld)),
+                         hs::pinned_staging(1, size_t(chunk * pld))};
+    if (!stage[0] || !stage[1]) return set_err(HS_ENOMEM, "pinned staging buffers");
+    cudaStream_t ss[2] = {s0, nullptr};
+    CK(cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking));
+    cudaEvent_t ev0 = nullptr, copied[2] = {nullptr, nullptr};
+    uint8_t *buf = nullptr;
+    hs_best *bests = nullptr;
+    int rc = HS_OK;
+    do {
+        cudaError_t e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+        for (auto &c : copied)
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&buf, 2 * per, s0);
+        if (e == cudaSuccess)
+            e = cudaMallocAsync((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
+        if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ss[1], ev0, 0);
+        if (e != cudaSuccess) {
+            rc = cuda_err(e, "hs_eval_host (packing) setup");
+            break;
+        }
+        for (int64_t c = 0; c < nchunks && rc == HS_OK; ++c) {
+            const int k = int(c & 1);
+            cudaStream_t s = ss[k];
+            uint8_t *b = buf + k * per;
+            double *dm = reinterpret_cast<double *>(b + ((gbytes + 255) & ~size_t(255)));
+            uint8_t *dsx = reinterpret_cast<uint8_t *>(dm + chunk);
+            const int64_t lo = c * chunk, rows = std::min(chunk, n - lo);
+            // the staging buffer's previous copy (chunk c-2) has left it
+            if (c >= 2) {
+                e = cudaEventSynchronize(copied[k]);
+                if (e != cudaSuccess) {
+                    rc = cuda_err(e, "staging reuse");
+                    break;
+                }
+            }
+            const bool ok = hs::pack2_rows(h_genes + lo * ld, ld, V, p.K, rows, stage[k], pld);
+            if (ok)
+                e = cudaMemcpyAsync(b, stage[k], size_t(rows * pld), cudaMemcpyHostToDevice, s);
+            else
+                e = cudaMemcpyAsync(b, h_genes + lo * ld, size_t((rows - 1) * ld + V),
+                                    cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaEventRecord(copied[k], s);
+            if (e != cudaSuccess) {
+                rc = cuda_err(e, "H2D genes");
+                break;
+            }
+            rc = run_eval(plan, b, rows, ok ? pld : ld, 0, 0, 0, nullptr, nullptr, 0,
+                          h_makespan ? dm : nullptr, h_status ? dsx : nullptr, nullptr,
+                          nullptr, h_best ? bests + c : nullptr, index_base + lo, s,
+                          ok ? 1 : 0);
+            if (rc) break;
+            if (h_makespan)
+                e = cudaMemcpyAsync(h_makespan + lo, dm, size_t(rows) * 8,
+                                    cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess && h_status)
+                e = cudaMemcpyAsync(h_status + lo, dsx, size_t(rows), cudaMemcpyDeviceToHost,
+                                    s);
+            if (e != cudaSuccess) rc = cuda_err(e, "D2H results");
+        }
+        if (rc) break;
+        e = cudaEventRecord(ev0, ss[1]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, ev0, 0);
+        std::vector<hs_best> hb(static_cast<size_t>(nchunks));
+        if (e == cudaSuccess && h_best)
+            e = cudaMemcpyAsync(hb.data(), bests, size_t(nchunks) * sizeof(hs_best),
+                                cudaMemcpyDeviceToHost, s0);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s0);
+        if (e != cudaSuccess) {
+            rc = cuda_err(e, "hs_eval_host sync");
+            break;
+        }
+        if (h_best) hs_best_merge(hb.data(), nchunks, h_best);
+    } while (0);
+    if (buf) cudaFreeAsync(buf, s0);
+    if (bests) cudaFreeAsync(bests, s0);
+    cudaStreamSynchronize(ss[1]);
+    cudaStreamSynchronize(s0);  // staging buffers are reused by the next call
+    cudaStreamDestroy(ss[1]);
+    if (ev0) cudaEventDestroy(ev0);
+    for (auto c : copied)
+        if (c) cudaEventDestroy(c);
+    return rc;
+}
+
+bool host_pack_enabled(const hs::Plan &p, int64_t n, int packed) {
+    if (packed || p.batched || p.K > 4 || p.V < 16 || n <= kSmallN) return false;
+    const int64_t pld = ((p.V + 3) / 4 + 3) / 4 * 4;
+    if (pld > p.pref_ld() || pld > 256) return false;
+    const char *v = getenv("HS_HOST_PACK");
+    return !v || std::atoi(v) != 0;
+}
+
 }  // namespace
 
 static int eval_host_impl(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
@@ -746,6 +858,9 @@ static int eval_host_impl(const hs_plan *plan, const uint8_t *h_genes, int64_t n
     if (n > 0 && n <= kSmallN && plan->p.V > 0)
         return eval_host_small(plan, h_genes, n, ld, h_makespan, h_status, h_best,
                                index_base, s0, packed);
+    if (host_pack_enabled(plan->p, n, packed))
+        return eval_host_u8_packed(plan, h_genes, n, ld, h_makespan, h_status, h_best,
+                                   index_base, s0);
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 1 << 19));
     const int64_t nchunks = n > 0 ? (n + chunk - 1) / chunk : 1;
     const size_t gbytes = size_t(chunk * ld);

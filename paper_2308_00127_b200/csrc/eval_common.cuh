@@ -171,6 +171,12 @@ __device__ __forceinline__ void tm_st2(hs_u32 addr, double v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};"
                  ::"r"(addr), "r"(__double2loint(v)), "r"(__double2hiint(v)) : "memory");
 }
+// end time + producer device (4 columns: lo, hi, device, unused)
+__device__ __forceinline__ void tm_st4(hs_u32 addr, double v, int dev) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %3};"
+                 ::"r"(addr), "r"(__double2loint(v)), "r"(__double2hiint(v)), "r"(dev)
+                 : "memory");
+}
 __device__ __forceinline__ void tm_ld2(hs_u32 addr, hs_u32 &lo, hs_u32 &hi) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
                  : "=r"(lo), "=r"(hi) : "r"(addr) : "memory");

@@ -1,0 +1,187 @@
+// Host-side packing for hs_eval_host: uint8 genomes in the reference's
+// layout (one byte per gene) are packed to 2 bits per gene by a pool of
+// host threads into pinned staging buffers while the GPU evaluates the
+// previous chunk, so the PCIe link carries ceil(V/4) bytes per candidate
+// instead of V (the host path is PCIe-bound). Genes >= K are detected on
+// the way (the caller then sends that chunk unpacked, where the kernel
+// flags them exactly as before).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "host_pack.hpp"
+
+namespace hs {
+namespace {
+
+// A fixed pool of worker threads running index ranges of one job at a time.
+class Pool {
+  public:
+    explicit Pool(int n) {
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : workers_) t.join();
+    }
+    int size() const { return int(workers_.size()) + 1; }
+    // fn(part) for part in [0, parts), the caller thread taking part too
+    void run(int parts, const std::function<void(int)> &fn) {
+        std::unique_lock<std::mutex> lk(job_m_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> g(m_);
+            fn_ = &fn;
+            parts_ = parts;
+            next_.store(0);
+            pending_ = parts;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> g(m_);
+        done_cv_.wait(g, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+  private:
+    void work() {
+        for (;;) {
+            const int k = next_.fetch_add(1);
+            if (k >= parts_) return;
+            (*fn_)(k);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_, job_m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)> *fn_ = nullptr;
+    std::atomic<int> next_{0};
+    int parts_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+Pool &pool() {
+    static Pool p([] {
+        int n = int(std::thread::hardware_concurrency());
+        if (const char *v = getenv("HS_HOST_THREADS")) n = std::atoi(v);
+        return std::max(0, std::min(n, 64) - 1);
+    }());
+    return p;
+}
+
+constexpr uint64_t kLow7 = 0x7F7F7F7F7F7F7F7Full, kHigh = 0x8080808080808080ull;
+
+// 2-bit packing of one row: genes 4j..4j+3 -> byte j (gene 4j+q in bits
+// 2q); returns nonzero when a gene is >= K
+inline uint64_t pack_row(const uint8_t *src, int V, uint8_t *dst, int pld, uint64_t kadd) {
+    uint64_t bad = 0;
+    int i = 0, o = 0;
+    for (; i + 8 <= V; i += 8, o += 2) {
+        uint64_t x;
+        std::memcpy(&x, src + i, 8);
+        bad |= (x & kHigh) | (((x & kLow7) + kadd) & kHigh);
+        // bytes b0..b7 (each < 4): y byte k = b_k | b_{k+1} << 2, then
+        // z byte 0 = b0 | b1 << 2 | b2 << 4 | b3 << 6 (byte 4 likewise)
+        const uint64_t y = x | (x >> 6);
+        const uint64_t z = y | (y >> 12);
+        dst[o] = uint8_t(z);
+        dst[o + 1] = uint8_t(z >> 32);
+    }
+    uint32_t acc = 0;
+    int sh = 0;
+    for (; i < V; ++i) {
+        const uint8_t b = src[i];
+        bad |= (uint64_t(b) & 0x80) | ((uint64_t(b & 0x7F) + (kadd & 0xFF)) & 0x80);
+        acc |= uint32_t(b & 3) << sh;
+        sh += 2;
+        if (sh == 8) {
+            dst[o++] = uint8_t(acc);
+            acc = 0;
+            sh = 0;
+        }
+    }
+    if (sh) dst[o++] = uint8_t(acc);
+    for (; o < pld; ++o) dst[o] = 0;
+    return bad;
+}
+
+}  // namespace
+
+int host_pack_threads() { return pool().size(); }
+
+bool pack2_rows(const uint8_t *src, int64_t ld, int V, int K, int64_t rows, uint8_t *dst,
+                int64_t pld) {
+    const uint64_t kadd = uint64_t(0x80 - K) * 0x0101010101010101ull;
+    Pool &pl = pool();
+    const int parts = int(std::min<int64_t>(rows, int64_t(pl.size()) * 4));
+    if (parts <= 0) return true;
+    std::atomic<uint64_t> bad{0};
+    pl.run(parts, [&](int k) {
+        const int64_t a = rows * k / parts, b = rows * (k + 1) / parts;
+        uint64_t bd = 0;
+        for (int64_t r = a; r < b; ++r)
+            bd |= pack_row(src + r * ld, V, dst + r * pld, int(pld), kadd);
+        if (bd) bad.fetch_or(1);
+    });
+    return bad.load() == 0;
+}
+
+// pinned staging buffers, per calling thread (the C ABI is thread-safe)
+namespace {
+struct Staging {
+    void *p[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+    ~Staging() {
+        for (void *q : p)
+            if (q) cudaFreeHost(q);
+    }
+};
+thread_local Staging t_stage;
+}  // namespace
+
+uint8_t *pinned_staging(int which, size_t bytes) {
+    if (bytes > t_stage.bytes) {
+        for (void *&q : t_stage.p) {
+            if (q) cudaFreeHost(q);
+            q = nullptr;
+        }
+        t_stage.bytes = 0;
+        for (void *&q : t_stage.p)
+            if (cudaHostAlloc(&q, bytes, cudaHostAllocDefault) != cudaSuccess) {
+                q = nullptr;
+                return nullptr;
+            }
+        t_stage.bytes = bytes;
+    }
+    return static_cast<uint8_t *>(t_stage.p[which & 1]);
+}
+
+}  // namespace hs

@@ -137,6 +137,7 @@ JitOpts JitOpts::from_env() {
             if (k == "tmem") o.tmem = std::atoi(v.c_str()) != 0;
             if (k == "tlanes") o.tm_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "tregs") o.tm_regs = std::max(0, std::atoi(v.c_str()));
+            if (k == "tdev") o.tm_dev = std::atoi(v.c_str()) != 0;
             // emission-only (hs_plan_emit_specialized): TMEM columns per warp
             // group, normally chosen by jit_build
             if (k == "tcols") o.tm_cols = std::max(0, std::atoi(v.c_str()));
@@ -425,8 +426,10 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                 ? "e" + std::to_string(q)
                 : o.tmem ? "TV" + is + "_" + std::to_string(q)  // loaded by tm_loads()
                 : "E[" + std::to_string((long long)where[q] * T) + "]";
+            const bool tdev = o.tmem && o.tm_dev && !in_reg && !greg;
             const std::string gq = greg ? gexpr(q)
                 : in_reg ? "d" + std::to_string(q)
+                : tdev ? "TD" + is + "_" + std::to_string(q)  // device from TMEM
                 : "(int)g[" + std::to_string(q) + "]";
             const std::string x = "x" + is + "_" + std::to_string(k);
             if (dom) {
@@ -522,30 +525,48 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         // one wait, then each pair moved into a true 64-bit output (a double
         // assembled from two separately-tied registers costs ptxas a
         // register-pair copy before every 64-bit use)
+        // TMEM slot layout: {end lo, end hi} (2 columns per slot) or, with
+        // tm_dev, {end lo, end hi, device, -} (4 columns; one .x4 load)
+        const int cps = o.tm_dev ? 4 : 2;
         for (size_t c = 0; c < qs.size(); c += 8) {
             const size_t m = std::min(qs.size(), c + 8) - c;
             std::string body = "{\\n .reg .b32 ";
             for (size_t k = 0; k < m; ++k)
                 body += (k ? ", " : "") + std::string("l") + std::to_string(k) + ", h" +
-                        std::to_string(k);
+                        std::to_string(k) + (o.tm_dev ? ", x" + std::to_string(k) +
+                                                         ", y" + std::to_string(k) : "");
             body += ";\\n";
-            for (size_t k = 0; k < m; ++k)
-                body += " tcgen05.ld.sync.aligned.32x32b.x2.b32 {l" + std::to_string(k) + ", h" +
-                        std::to_string(k) + "}, [%" + std::to_string(m + k) + "];\\n";
+            const size_t no = o.tm_dev ? 2 * m : m;  // outputs: value (+ device) each
+            for (size_t k = 0; k < m; ++k) {
+                const std::string ks = std::to_string(k);
+                body += o.tm_dev
+                    ? " tcgen05.ld.sync.aligned.32x32b.x4.b32 {l" + ks + ", h" + ks + ", x" + ks +
+                          ", y" + ks + "}, [%" + std::to_string(no + k) + "];\\n"
+                    : " tcgen05.ld.sync.aligned.32x32b.x2.b32 {l" + ks + ", h" + ks + "}, [%" +
+                          std::to_string(no + k) + "];\\n";
+            }
             body += " tcgen05.wait::ld.sync.aligned;\\n";
-            for (size_t k = 0; k < m; ++k)
-                body += " mov.b64 %" + std::to_string(k) + ", {l" + std::to_string(k) + ", h" +
-                        std::to_string(k) + "};\\n";
+            for (size_t k = 0; k < m; ++k) {
+                const std::string ks = std::to_string(k);
+                body += " mov.b64 %" + ks + ", {l" + ks + ", h" + ks + "};\\n";
+                if (o.tm_dev) body += " mov.b32 %" + std::to_string(m + k) + ", x" + ks + ";\\n";
+            }
             body += "}";
-            std::string outs, ins;
+            std::string outs, outs_d, ins;
             for (size_t k = 0; k < m; ++k) {
                 const std::string v = "TV" + is + "_" + std::to_string(qs[c + k]);
                 s += "    double " + v + ";\n";
                 outs += std::string(k ? ", " : "") + "\"=d\"(" + v + ")";
+                if (o.tm_dev) {
+                    const std::string dv = "TD" + is + "_" + std::to_string(qs[c + k]);
+                    s += "    int " + dv + ";\n";
+                    outs_d += ", \"=r\"(" + dv + ")";
+                }
                 ins += std::string(k ? ", " : "") + "\"r\"(TB + " +
-                       std::to_string(2 * where[qs[c + k]]) + "u)";
+                       std::to_string(cps * where[qs[c + k]]) + "u)";
             }
-            s += "    asm volatile(\"" + body + "\" : " + outs + " : " + ins + " : \"memory\");\n";
+            s += "    asm volatile(\"" + body + "\" : " + outs + outs_d + " : " + ins +
+                 " : \"memory\");\n";
         }
     };
     auto head = [&](int i) {
@@ -661,7 +682,10 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                  ";\n";
         }
         if (where[i] >= 0) {
-            if (o.tmem)
+            if (o.tmem && o.tm_dev)
+                s += "    tm_st4(TB + " + std::to_string(4 * where[i]) + ", " + stored + ", " + di +
+                     ");\n";
+            else if (o.tmem)
                 s += "    tm_st2(TB + " + std::to_string(2 * where[i]) + ", " + stored + ");\n";
             else
                 s += "    E[" + std::to_string((long long)where[i] * T) + "] = " + stored + ";\n";
@@ -936,7 +960,10 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
         const bool dt = lanes_t(true) >= lanes_t(false);
         const int Tt = std::min(lanes_t(dt), 512);
         const int groups = (Tt / 32 + 3) / 4;
-        const int cols = groups > 0 ? (512 / groups) & ~1 : 0;
+        // column bands 4-aligned (the .x4 slot accesses start on them)
+        const int cols = groups > 0 ? (512 / groups) & ~3 : 0;
+        if (Tt >= 32 && slots_t > 0 && (ot.tm_dev ? 4 : 2) * slots_t > cols)
+            ot.tm_dev = false;  // the device column does not fit: end times only
         if (Tt >= 32 && slots_t > 0 && 2 * slots_t <= cols) {
             oe = ot;
             oe.tm_cols = cols;

@@ -36,6 +36,11 @@ struct JitOpts {
     int tm_lanes = 384;       // lanes per CTA with TMEM slots (12 warps)
     int tm_regs = 40;         // long-lived end times in registers with TMEM slots
     int tm_cols = 0;          // (set by jit_build) TMEM columns per warp group
+    bool tm_dev = false;      // TMEM slots also hold the producer's device
+                              // (4 columns per slot: the consumer's device
+                              // compare needs no shared-memory gene load);
+                              // measured neutral on WS200, -3 % on the WS
+                              // 10x20 stack (profiles r2e), so off
     int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
     static JitOpts from_env();
 };

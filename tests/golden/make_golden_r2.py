@@ -273,19 +273,24 @@ def _save_lat(t):
 
 # ------------------------------------------------------------ lower bounds
 def _lb_job(args):
+    from hetsched.core import save_hardware, save_latency
     name, L, workers = args
-    g, hw, t = load(name)
+    g, d0, hw, t = benchgen.gen_stacked_instance(*name)
     d = k_edge_components(g, 1)
     rep = lower_bound(g, hw, t, L, d, workers=workers)
-    return {"instance": name, "L": L, "subgraph_cap": 40,
+    return {"instance": "gen_stacked_instance%r" % (name,), "L": L,
+            "subgraph_cap": 40, "graph": json.loads(save_graph(g)),
+            "hardware": json.loads(save_hardware(hw)),
+            "latency": json.loads(save_latency(t)),
             "lower_bound_ms": fhex(rep.lower_bound_ms),
             "throughput_upper_bound": fhex(rep.throughput_upper_bound),
             "terms": json.loads(json.dumps(rep.terms))}
 
 
 def bounds_doc():
-    jobs = [("er_stack_10x10", 1, 1), ("er_stack_10x10", 2, 1),
-            ("er_stack_4x10_c2", 1, 1), ("ws_stack_10x20", 1, 1)]
+    # small stacks: the MILP sub-solves of a 24-task instance already take
+    # ~80 s single-threaded (HiGHS), the 10-module stacks hours
+    jobs = [(("er", 6, 3, 1, "sdep", 0), 1, 8)]
     with get_context("fork").Pool(len(jobs)) as p:
         return p.map(_lb_job, jobs, chunksize=1)
 

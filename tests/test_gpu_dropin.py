@@ -96,19 +96,19 @@ def _cap40():
 
 
 @pytest.mark.parametrize("e", _cap40(),
-                         ids=lambda e: f"{e['instance']}_L{e['L']}")
+                         ids=lambda e: f"stack_L{e['L']}")
 def test_lower_bound_default_cap(ref, e):
     """cap = 40: the reference's lower_bound on the B200 building blocks
     (patched) and this package's lower_bound with the reference MILP as its
     explicit sub-solver, run 8 sub-solves at a time -- both equal the
     reference's unpatched result."""
     from paper_2308_00127_b200.bounds import reference_milp_solver
-    rg, rhw, rt = _ref_inst(ref, instance_doc(e["instance"]))
+    rg, rhw, rt = _ref_inst(ref, e)
     rd = ref["split"].k_edge_components(rg, 1)
     rep = ref["bounds"].lower_bound(rg, rhw, rt, e["L"], rd, workers=8)
     assert fhex(rep.lower_bound_ms) == e["lower_bound_ms"]
     assert json.loads(json.dumps(rep.terms)) == e["terms"]
-    g, hw, t = hs.load_instance(instance_doc(e["instance"]))
+    g, hw, t = hs.load_instance(e)
     mine = hs.lower_bound(g, hw, t, e["L"], hs.k_edge_components(g, 1),
                           workers=8, milp=reference_milp_solver())
     assert fhex(mine.lower_bound_ms) == e["lower_bound_ms"]

@@ -62,6 +62,21 @@ if "search" in which:
         a = hs.simulated_annealing(g, hw, t, 1, seed=0, budget=300)
         b = hs.one_plus_one_ea(g, hw, t, 1, seed=0, budget=300)
         print("search", name, a.objective, b.objective)
+if "sa_only" in which:
+    # hs_jit_sa in a process where no kernel with an mbarrier ran before
+    # (start fitness from the CPU oracle instead of a GPU evaluation)
+    from paper_2308_00127_b200.heuristics import _sa_device_chain
+    d = doc("ws30")
+    g, hw, t = hs.load_instance(d)
+    plan = get_plan(g, hw, t, 1)
+    plan.specialize()
+    genes = np.zeros(plan.V, np.uint8)
+    f0, _ = O.fitness_np(O.build_tables(O.Instance.from_doc(d), 1),
+                         genes[None, :])
+    best, bf = _sa_device_chain(plan, np.random.default_rng(0), genes,
+                                float(f0[0]), float(f0[0]), 0.1 * float(f0[0]),
+                                0.995, 300, plan.K, 128)
+    print("sa_only", bf)
 if "aot" in which:
     check("ws30", 20000, False)
     check("tf96", 5000, False)
