@@ -29,6 +29,6 @@ from .batched import (batched_genes_from_schedule, batched_options,
                       decode_batched, fitness_batched, random_search_batched)
 from .validate import validate_schedule, validate_schedules
 from .modularity import (decomposition_modularity, modularity,
-                         modularity_batch)
+                         modularity_batch, modularity_split)
 
 __version__ = "0.1.0"

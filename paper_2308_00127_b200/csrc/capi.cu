@@ -734,12 +734,15 @@ int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     return HS_OK;
 }
 
-// uint8 host genomes (the reference's layout), K <= 4: the host thread pool
-// packs each chunk to 2 bits per gene into a pinned staging buffer while
-// the GPU copies and evaluates the previous one (double-buffered), so the
-// PCIe link -- the bound of this path -- carries ceil(V/4) instead of V
-// bytes per candidate. A chunk holding a gene >= K goes over unpacked, so
-// the kernel flags it (status 5) exactly as on the unpacked path.
+// uint8 host genomes (the reference's layout), K <= 4, HS_HOST_PACK=1: the
+// host thread pool packs each chunk to 2 bits per gene into a pinned
+// staging buffer while the GPU copies and evaluates the previous one
+// (double-buffered), so the PCIe link carries ceil(V/4) instead of V bytes
+// per candidate. It pays only where the host threads read memory faster
+// than the copy engine does (not on this pool's 16-vCPU hosts: 1.3e8 vs
+// 2.7e8 candidates/s, profiles r2f), hence opt-in. A chunk holding a gene
+// >= K goes over unpacked, so the kernel flags it (status 5) exactly as on
+// the unpacked path.
 int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, int64_t ld,
                         double *h_makespan, uint8_t *h_status, hs_best *h_best,
                         int64_t index_base, cudaStream_t s0) {
@@ -841,8 +844,10 @@ bool host_pack_enabled(const hs::Plan &p, int64_t n, int packed) {
     if (packed || p.batched || p.K > 4 || p.V < 16 || n <= kSmallN) return false;
     const int64_t pld = ((p.V + 3) / 4 + 3) / 4 * 4;
     if (pld > p.pref_ld() || pld > 256) return false;
+    // opt-in: on the pool's hosts the CPU threads read the uint8 rows at
+    // ~27 GB/s while the copy engine reads them at ~54 GB/s (profiles r2f)
     const char *v = getenv("HS_HOST_PACK");
-    return !v || std::atoi(v) != 0;
+    return v && std::atoi(v) != 0;
 }
 
 }  // namespace

@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <immintrin.h>
+
 #include "host_pack.hpp"
 
 namespace hs {
@@ -133,6 +135,36 @@ inline uint64_t pack_row(const uint8_t *src, int V, uint8_t *dst, int pld, uint6
     return bad;
 }
 
+// AVX2: 32 genes -> 8 bytes per step (maddubs pairs b0 + 4 b1, madd quads
+// (b0 + 4 b1) + 16 (b2 + 4 b3), then 32 -> 16 -> 8-bit packs); genes >= K
+// found by an unsigned max over the row
+__attribute__((target("avx2"))) uint64_t pack_row_avx2(const uint8_t *src, int V,
+                                                         uint8_t *dst, int pld, uint64_t kadd,
+                                                         int K) {
+    const __m256i m14 = _mm256_set1_epi16(0x0401);   // bytes (1, 4)
+    const __m256i m116 = _mm256_set1_epi32(0x00100001);  // words (1, 16)
+    __m256i mx = _mm256_setzero_si256();
+    int i = 0, o = 0;
+    for (; i + 32 <= V; i += 32, o += 8) {
+        const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+        mx = _mm256_max_epu8(mx, x);
+        const __m256i p = _mm256_maddubs_epi16(x, m14);  // 16 x (b0 + 4 b1)
+        const __m256i q = _mm256_madd_epi16(p, m116);    // 8 x packed byte in int32
+        const __m256i w = _mm256_packus_epi32(q, q);     // per 128-bit half
+        const __m256i b = _mm256_packus_epi16(w, w);
+        const uint32_t lo = uint32_t(_mm256_cvtsi256_si32(b));
+        const uint32_t hi = uint32_t(_mm256_extract_epi32(b, 4));
+        std::memcpy(dst + o, &lo, 4);
+        std::memcpy(dst + o + 4, &hi, 4);
+    }
+    alignas(32) uint8_t m[32];
+    _mm256_store_si256(reinterpret_cast<__m256i *>(m), mx);
+    uint64_t bad = 0;
+    for (int k = 0; k < 32; ++k) bad |= m[k] >= K;
+    // the rest (< 32 genes) by the scalar code, byte aligned (i % 4 == 0)
+    return bad | pack_row(src + i, V - i, dst + o, pld - o, kadd);
+}
+
 }  // namespace
 
 int host_pack_threads() { return pool().size(); }
@@ -140,6 +172,7 @@ int host_pack_threads() { return pool().size(); }
 bool pack2_rows(const uint8_t *src, int64_t ld, int V, int K, int64_t rows, uint8_t *dst,
                 int64_t pld) {
     const uint64_t kadd = uint64_t(0x80 - K) * 0x0101010101010101ull;
+    static const bool avx2 = __builtin_cpu_supports("avx2");
     Pool &pl = pool();
     const int parts = int(std::min<int64_t>(rows, int64_t(pl.size()) * 4));
     if (parts <= 0) return true;
@@ -147,8 +180,12 @@ bool pack2_rows(const uint8_t *src, int64_t ld, int V, int K, int64_t rows, uint
     pl.run(parts, [&](int k) {
         const int64_t a = rows * k / parts, b = rows * (k + 1) / parts;
         uint64_t bd = 0;
-        for (int64_t r = a; r < b; ++r)
-            bd |= pack_row(src + r * ld, V, dst + r * pld, int(pld), kadd);
+        if (avx2)
+            for (int64_t r = a; r < b; ++r)
+                bd |= pack_row_avx2(src + r * ld, V, dst + r * pld, int(pld), kadd, K);
+        else
+            for (int64_t r = a; r < b; ++r)
+                bd |= pack_row(src + r * ld, V, dst + r * pld, int(pld), kadd);
         if (bd) bad.fetch_or(1);
     });
     return bad.load() == 0;

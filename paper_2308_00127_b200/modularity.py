@@ -69,3 +69,54 @@ def modularity(g, communities: Sequence, resolution: float = 1.0) -> float:
 def decomposition_modularity(g, decomposition, resolution: float = 1.0):
     """Score of a ModuleDecomposition (its modules as communities)."""
     return modularity(g, list(decomposition.modules), resolution)
+
+
+def _labels(ids: list, modules: Sequence) -> np.ndarray:
+    pos = {t: k for k, t in enumerate(ids)}
+    lab = np.empty(len(ids), np.int32)
+    for c, m in enumerate(modules):
+        for t in m:
+            lab[pos[t]] = c
+    return lab
+
+
+def modularity_split(g, c: int = 1, resolution: float = 1.0,
+                     max_merges: int | None = None):
+    """The modularity score driving the split: start from the reference's
+    module detection (``k_edge_components(g, c)``, splitting.py:178-219) and
+    greedily merge the pair of topologically consecutive modules whose union
+    raises the Newman modularity of the partition the most -- every
+    candidate merge of a round scored in one K7 launch -- until no merge
+    raises it. Merging consecutive modules of a topological order keeps the
+    module digraph acyclic, so the result is again a ModuleDecomposition
+    the split DP (milp_split) accepts: fewer, larger modules where the
+    channels between them carried little of the graph's edge weight.
+    Returns (decomposition, modularity)."""
+    from .splitting import ModuleDecomposition, k_edge_components
+    d = k_edge_components(g, c)
+    mods = [frozenset(m) for m in d.modules]
+    ids = list(g.tasks)
+    cur = float(modularity_batch(g, _labels(ids, mods)[None, :],
+                                 n_comm=max(len(mods), 1),
+                                 resolution=resolution)[0]) if mods else 0.0
+    merges = 0
+    while len(mods) > 1 and (max_merges is None or merges < max_merges):
+        cands = []
+        for t in range(len(mods) - 1):
+            cands.append(mods[:t] + [mods[t] | mods[t + 1]] + mods[t + 2:])
+        lab = np.stack([_labels(ids, m) for m in cands])
+        q = modularity_batch(g, lab, n_comm=len(mods) - 1,
+                             resolution=resolution)
+        k = int(np.argmax(q))  # first maximum: the earliest pair
+        if not q[k] > cur:
+            break
+        mods, cur = cands[k], float(q[k])
+        merges += 1
+    module_of = {t: k for k, m in enumerate(mods) for t in m}
+    cuts: dict = {}
+    for a, b in g.edges:
+        ma, mb = module_of[a], module_of[b]
+        if ma != mb:
+            cuts.setdefault((ma, mb), []).append((a, b))
+    return ModuleDecomposition(modules=mods, cut_edges=cuts, channels=c,
+                               is_chain=all(b == a + 1 for (a, b) in cuts)), cur
