@@ -248,7 +248,11 @@ def run_reference(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (uniform random genomes; reference benchgen "
                    "graph frozen as JSON)",
-           "config": _config(per_step, 1),
+           # the same workload description as the GPU arm (each timed step
+           # here scores a bounded sample of it: cpu_baseline.sample)
+           "config": _config(args.n, args.gpus),
+           "evaluator": "hetsched.heuristics.fitness (the reference, "
+                        "unmodified), warm fork pool on the host cores",
            "cpu_baseline": {
                "value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                "sample": f"{per_step} uniform WS200 genomes per step, "
@@ -521,6 +525,22 @@ def split_config3():
                     "reference_heft_ms": 2263.1,
                     "reference_lower_bound_cap40_ms": 1878.24,
                     "source": "SURVEY.md 3(3) / 6 (survey-measured, CPU)"}})
+    # the 1000-node stack (V=1020): split with sampled module sweeps
+    g, hw, t = hs.load_instance(_inst("ws_stack_10x100"))
+    t0 = time.perf_counter()
+    dec = hs.k_edge_components(g, 1)
+    sched = hs.milp_split(g, hw, t, 1, dec,
+                          module_solver=hs.gpu_module_solver(), workers=8)
+    t1 = time.perf_counter()
+    mk = hs.validate_schedule(g, hw, t, sched)
+    lb = hs.lower_bound(g, hw, t, 1, dec, subgraph_cap=0)
+    out["ws_stack_10x100"] = {
+        "instance": "ws_stack_10x100 (V=1020, 10 modules)",
+        "modules": len(dec.modules), "split_s": t1 - t0,
+        "objective_ms": sched.objective, "validated_makespan_ms": mk,
+        "lower_bound_ms": lb.lower_bound_ms,
+        "gap": sched.objective / lb.lower_bound_ms - 1.0
+        if lb.lower_bound_ms > 0 else None}
     return out
 
 
@@ -819,10 +839,10 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (uniform random genomes; "
                                 "reference benchgen graph frozen as JSON)",
-        "config": {**_config(n, world),
-                   "evaluator": ("graph-specialised (NVRTC sm_100a, compiled "
-                                 f"once in {jit_ms:.0f} ms, not timed)")
-                   if jit_ms is not None else "ahead-of-time plan walker"},
+        "config": _config(n, world),
+        "evaluator": ("graph-specialised hs_jit_eval (NVRTC sm_100a, compiled "
+                      f"once in {jit_ms:.0f} ms, not timed)")
+        if jit_ms is not None else "ahead-of-time plan walker",
         "best": {"cost_ms": bcost, "index": bidx},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
@@ -896,6 +916,29 @@ def cpu_legs(doc, d_genes, d_ms, sweep_samples, tts):
         out["c_port_all_cores"] = {"error": repr(exc)}
     if isinstance(tts, dict) and "error" not in tts:
         out["time_to_solution"] = reference_search(tts)
+    try:
+        out["split_comparators"] = reference_constructive()
+    except Exception as exc:
+        out["split_comparators"] = {"error": repr(exc)}
+    return out
+
+
+def reference_constructive():
+    """The reference's own HEFT and greedy (heuristics.py:192-256) on the
+    split instances, as the comparators of the GPU split's objective."""
+    from oracle import ref
+    ref.import_reference()
+    RH = sys.modules["hetsched.heuristics"]
+    out = {}
+    for name in ("ws_stack_10x20", "ws_stack_10x100"):
+        g, hw, t = ref.load_instance(_inst(name))
+        row = {}
+        for algo in ("heft", "greedy"):
+            t0 = time.perf_counter()
+            s = getattr(RH, algo)(g, hw, t, 1)
+            row[algo] = {"objective_ms": s.objective,
+                         "s": time.perf_counter() - t0}
+        out[name] = row
     return out
 
 

@@ -185,10 +185,14 @@ def _groups(order, devs, pins, same_device):
 def gpu_module_solver(objective: str = "latency", *,
                       exhaustive_limit: int = 1 << 24,
                       samples: int = 1 << 22, refine_rounds: int = 64,
+                      starts: int = 8, pair_moves: bool = True,
                       seed: int = 0) -> ModuleSolver:
     """Build a ModuleSolver (see module docstring). `objective` is accepted
     for signature parity: latency and throughput share the makespan
-    (milp.py:144-146)."""
+    (milp.py:144-146). Sampled modules are refined by a batched multi-start
+    local search: the `starts` best samples move together, each round
+    evaluating every single-group and (with `pair_moves`) every two-group
+    reassignment of every incumbent in one GPU batch, until none improves."""
     if objective not in ("latency", "throughput"):
         raise ValueError(f"unknown objective {objective!r}")
 
@@ -212,26 +216,42 @@ def gpu_module_solver(objective: str = "latency", *,
         total = space if mode == N.GEN_ENUM else samples
         chunk = 1 << 22
         found = (float("inf"), -1)
+        pool = []  # (cost, index) of the best samples (random mode)
+        ms_buf = torch.empty(min(chunk, total), dtype=torch.float64,
+                             device="cuda") if mode == N.GEN_RANDOM else None
         for lo in range(0, total, chunk):
             m = min(chunk, total - lo)
             plan.eval_gen(mode, seed, lo, m, template=d_t, group=d_g,
-                          n_groups=ng, best=best)
+                          n_groups=ng, best=best,
+                          makespan=ms_buf[:m] if ms_buf is not None else None)
             b = best.cpu()
             c = (float(b[:1].view(torch.float64).item()), int(b[1].item()))
             if c < found:
                 found = c
+            if ms_buf is not None and starts > 1:
+                k = min(starts, m)
+                v, ix = torch.topk(ms_buf[:m], k, largest=False, sorted=True)
+                pool += [(float(a), lo + int(j)) for a, j in
+                         zip(v.cpu().tolist(), ix.cpu().tolist())]
             if deadline is not None and time.monotonic() > deadline:
                 break
         if found[1] < 0:
             return None, None, False
+        idx = [found[1]]
+        if pool:
+            pool.sort()
+            idx = [j for c, j in pool[:starts] if np.isfinite(c)] or idx
+        rows = np.empty((len(idx), V), np.uint8)
         out = torch.empty((1, V), dtype=torch.uint8, device="cuda")
-        plan.eval_gen(mode, seed, found[1], 1, template=d_t, group=d_g,
-                      n_groups=ng, genes_out=out)
-        genes = out.cpu().numpy()[0].copy()
+        for r, j in enumerate(idx):
+            plan.eval_gen(mode, seed, j, 1, template=d_t, group=d_g,
+                          n_groups=ng, genes_out=out)
+            rows[r] = out.cpu().numpy()[0]
+        genes = rows[0].copy()
         cost = found[0]
         if mode == N.GEN_RANDOM and np.isfinite(cost):
-            genes, cost = _refine(plan, genes, cost, group, K,
-                                  refine_rounds, deadline)
+            genes, cost = _refine_multi(plan, rows, group, K, refine_rounds,
+                                        pair_moves, deadline)
         if not np.isfinite(cost):
             return None, None, False
         sched = decode(MappingGenome(genes=tuple(int(x) for x in genes),
@@ -243,30 +263,69 @@ def gpu_module_solver(objective: str = "latency", *,
     return solver
 
 
-def _refine(plan, genes, cost, group, K, rounds, deadline):
-    """Best-improvement 1-opt over free groups, one GPU batch per round."""
+def _refine_multi(plan, rows, group, K, rounds, pairs, deadline):
+    """Best-improvement local search of several incumbents at once: each
+    round evaluates, in one GPU batch, every reassignment of one free group
+    (and, with `pairs`, of two) of every incumbent; each incumbent moves to
+    its best improving neighbour (first index on ties); the search ends when
+    none improves. Returns the best (genes, cost), ties to the earlier
+    incumbent."""
+    V = rows.shape[1]
     ng = int(group.max()) + 1 if (group >= 0).any() else 0
-    members = [np.flatnonzero(group == j) for j in range(ng)]
+    if ng == 0:
+        f = _fit_rows(plan, rows[:1])
+        return rows[0].copy(), float(f[0])
+    gm = np.zeros((ng, V), bool)  # group membership masks
+    gm[group[group >= 0], np.flatnonzero(group >= 0)] = True
+    first = np.array([np.flatnonzero(group == j)[0] for j in range(ng)])
+    j1 = np.repeat(np.arange(ng), K)
+    v1 = np.tile(np.arange(K), ng)
+    pairs = pairs and 1 < ng <= 48  # two-group moves: O(ng^2 K^2) rows
+    if pairs:
+        a, b = np.triu_indices(ng, 1)
+        ja = np.repeat(a, K * K)
+        jb = np.repeat(b, K * K)
+        va = np.tile(np.repeat(np.arange(K), K), len(a))
+        vb = np.tile(np.tile(np.arange(K), K), len(a))
+    inc = rows.copy()
+    cost = _fit_rows(plan, inc).astype(np.float64)
+    live = np.isfinite(cost)
     for _ in range(rounds):
-        rows, ok = [], []
-        for j in range(ng):
-            cur = genes[members[j][0]]
-            for k in range(K):
-                if k == cur:
-                    continue
-                r = genes.copy()
-                r[members[j]] = k
-                rows.append(r)
-        if not rows:
+        batch, owner = [], []
+        for s in np.flatnonzero(live):
+            g0 = inc[s]
+            cur = g0[first]
+            keep = v1 != cur[j1]
+            nb = np.where(gm[j1[keep]], v1[keep, None].astype(np.uint8),
+                          g0[None, :])
+            batch.append(nb)
+            owner.append(np.full(len(nb), s))
+            if pairs:
+                keep = (va != cur[ja]) & (vb != cur[jb])
+                nb = np.where(gm[ja[keep]], va[keep, None].astype(np.uint8),
+                              np.where(gm[jb[keep]],
+                                       vb[keep, None].astype(np.uint8),
+                                       g0[None, :]))
+                batch.append(nb)
+                owner.append(np.full(len(nb), s))
+        if not batch:
             break
-        fits = _fit_rows(plan, np.stack(rows))
-        k = int(np.argmin(fits))
-        if not fits[k] < cost:
+        cand = np.ascontiguousarray(np.concatenate(batch), np.uint8)
+        own = np.concatenate(owner)
+        f = _fit_rows(plan, cand)
+        moved = False
+        for s in np.flatnonzero(live):
+            sel = np.flatnonzero(own == s)
+            k = sel[int(np.argmin(f[sel]))]
+            if f[k] < cost[s]:
+                inc[s], cost[s] = cand[k], f[k]
+                moved = True
+            else:
+                live[s] = False
+        if not moved or (deadline is not None and time.monotonic() > deadline):
             break
-        genes, cost = rows[k], float(fits[k])
-        if deadline is not None and time.monotonic() > deadline:
-            break
-    return genes, cost
+    b = int(np.argmin(cost))
+    return inc[b].copy(), float(cost[b])
 
 
 # ---------------------------------------------------------------------------
