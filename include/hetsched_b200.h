@@ -271,6 +271,11 @@ int hs_eval_gen(const hs_plan *plan, uint64_t seed, int64_t first, int64_t n,
  * (splitting.py:225-245, pins and same_device of milp.py:277-291). */
 #define HS_GEN_RANDOM 1
 #define HS_GEN_ENUM 2
+/* HS_GEN_NEIGHBOR: the one- and two-group moves of the incumbent genome
+ * d_template (every position's gene): index c < n_groups*K sets group c/K
+ * to c%K; index n_groups*K + ((j*n_groups + l)*K + a)*K + b sets group j
+ * to a and, when l > j, group l to b (the module solver's local search). */
+#define HS_GEN_NEIGHBOR 3
 int hs_eval_gen_ex(const hs_plan *plan, int mode, uint64_t seed, int64_t first,
                    int64_t n, const uint8_t *d_template, const int16_t *d_group,
                    int32_t n_groups, double *d_makespan, uint8_t *d_status,

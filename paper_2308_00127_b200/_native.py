@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libhetsched_b200.so")
 HS_OK, HS_EINVAL, HS_ECYCLE, HS_ECUDA, HS_ENOMEM = 0, 1, 2, 3, 4
 ST_OK, ST_BATCH, ST_MEMORY, ST_LINK, ST_MISSING, ST_GENE = 0, 1, 2, 3, 4, 5
 
-GEN_RANDOM, GEN_ENUM = 1, 2
+GEN_RANDOM, GEN_ENUM, GEN_NEIGHBOR = 1, 2, 3
 
 _p = C.POINTER
 

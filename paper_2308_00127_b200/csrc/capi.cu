@@ -640,8 +640,15 @@ int hs_eval_gen_ex(const hs_plan *plan, int mode, uint64_t seed, int64_t first,
                    uint8_t *d_genes_out, hs_best *d_best, void *stream) {
     if (!plan) return set_err(HS_EINVAL, "null plan");
     if (first < 0) return set_err(HS_EINVAL, "first < 0");
-    if (mode != HS_GEN_RANDOM && mode != HS_GEN_ENUM)
+    if (mode != HS_GEN_RANDOM && mode != HS_GEN_ENUM && mode != HS_GEN_NEIGHBOR)
         return set_err(HS_EINVAL, "unknown generation mode");
+    if (mode == HS_GEN_NEIGHBOR) {
+        if (!d_group || !d_template || n_groups < 1)
+            return set_err(HS_EINVAL, "neighbour moves need a template and groups");
+        const long double k = plan->p.K, ng = n_groups;
+        if ((long double)first + (long double)n > ng * k + ng * ng * k * k)
+            return set_err(HS_EINVAL, "neighbour index out of range");
+    }
     if (d_group && (n_groups < 0 || n_groups > plan->p.V || !d_template))
         return set_err(HS_EINVAL, "group map needs a template and "
                                   "0 <= n_groups <= V");

@@ -365,6 +365,33 @@ static __device__ __noinline__ void reduce_best(double bc, hs_i64 bi, Best *part
 __device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 cidx) {
     const int NG = a.n_groups, K = a.gene_range, V = a.V;
     const hs_u64 c = (hs_u64)cidx;
+    if (a.gen == 3) {
+        // neighbours of the incumbent a.tmpl: index < NG*K moves one group
+        // (j -> va), the rest two groups ((j*NG + l)*K + va)*K + vb (j >= l
+        // leaves l alone); positions outside every group (group -1) keep
+        // the template, so "no second group" is -2
+        int j, l = -2, va, vb = 0;
+        const hs_u64 singles = (hs_u64)NG * (hs_u64)K;
+        if (c < singles) {
+            j = (int)(c / (hs_u64)K);
+            va = (int)(c % (hs_u64)K);
+        } else {
+            hs_u64 p = c - singles;
+            vb = (int)(p % (hs_u64)K);
+            p /= (hs_u64)K;
+            va = (int)(p % (hs_u64)K);
+            p /= (hs_u64)K;
+            l = (int)(p % (hs_u64)NG);
+            j = (int)(p / (hs_u64)NG);
+            if (l <= j) l = -2;
+        }
+        for (int q = 0; q < V; ++q) {
+            const int gq = a.group[q];
+            r8[q] = gq == j ? (hs_u8)va : (gq == l ? (hs_u8)vb : a.tmpl[q]);
+        }
+        for (int q = V; q < ((V + 3) & ~3); ++q) r8[q] = 0;
+        return;
+    }
     if (a.gen == 1) {
         const int W4 = (NG + 3) >> 2;
         hs_u32 *row = reinterpret_cast<hs_u32 *>(r8);

@@ -264,64 +264,52 @@ def gpu_module_solver(objective: str = "latency", *,
 
 
 def _refine_multi(plan, rows, group, K, rounds, pairs, deadline):
-    """Best-improvement local search of several incumbents at once: each
-    round evaluates, in one GPU batch, every reassignment of one free group
-    (and, with `pairs`, of two) of every incumbent; each incumbent moves to
-    its best improving neighbour (first index on ties); the search ends when
-    none improves. Returns the best (genes, cost), ties to the earlier
-    incumbent."""
-    V = rows.shape[1]
+    """Best-improvement local search of several incumbents: each round, for
+    every incumbent, one launch evaluates all of its one-group and (with
+    `pairs`) two-group reassignments, generated on the device
+    (HS_GEN_NEIGHBOR) and reduced by the fused first-index argmin; the
+    incumbent moves to that neighbour if it improves, else it is done.
+    Returns the best (genes, cost), ties to the earlier incumbent."""
+    import torch
     ng = int(group.max()) + 1 if (group >= 0).any() else 0
-    if ng == 0:
-        f = _fit_rows(plan, rows[:1])
-        return rows[0].copy(), float(f[0])
-    gm = np.zeros((ng, V), bool)  # group membership masks
-    gm[group[group >= 0], np.flatnonzero(group >= 0)] = True
-    first = np.array([np.flatnonzero(group == j)[0] for j in range(ng)])
-    j1 = np.repeat(np.arange(ng), K)
-    v1 = np.tile(np.arange(K), ng)
-    pairs = pairs and 1 < ng <= 48  # two-group moves: O(ng^2 K^2) rows
-    if pairs:
-        a, b = np.triu_indices(ng, 1)
-        ja = np.repeat(a, K * K)
-        jb = np.repeat(b, K * K)
-        va = np.tile(np.repeat(np.arange(K), K), len(a))
-        vb = np.tile(np.tile(np.arange(K), K), len(a))
-    inc = rows.copy()
+    inc = np.ascontiguousarray(rows, np.uint8).copy()
     cost = _fit_rows(plan, inc).astype(np.float64)
+    if ng == 0:
+        return inc[0].copy(), float(cost[0])
+    pairs = pairs and 1 < ng <= 512
+    M = ng * K + (ng * ng * K * K if pairs else 0)
+    d_group = torch.from_numpy(np.ascontiguousarray(group, np.int16)).cuda()
+    d_tmpl = torch.empty(inc.shape[1], dtype=torch.uint8, device="cuda")
+    best = torch.empty(2, dtype=torch.int64, device="cuda")
     live = np.isfinite(cost)
     for _ in range(rounds):
-        batch, owner = [], []
-        for s in np.flatnonzero(live):
-            g0 = inc[s]
-            cur = g0[first]
-            keep = v1 != cur[j1]
-            nb = np.where(gm[j1[keep]], v1[keep, None].astype(np.uint8),
-                          g0[None, :])
-            batch.append(nb)
-            owner.append(np.full(len(nb), s))
-            if pairs:
-                keep = (va != cur[ja]) & (vb != cur[jb])
-                nb = np.where(gm[ja[keep]], va[keep, None].astype(np.uint8),
-                              np.where(gm[jb[keep]],
-                                       vb[keep, None].astype(np.uint8),
-                                       g0[None, :]))
-                batch.append(nb)
-                owner.append(np.full(len(nb), s))
-        if not batch:
-            break
-        cand = np.ascontiguousarray(np.concatenate(batch), np.uint8)
-        own = np.concatenate(owner)
-        f = _fit_rows(plan, cand)
         moved = False
         for s in np.flatnonzero(live):
-            sel = np.flatnonzero(own == s)
-            k = sel[int(np.argmin(f[sel]))]
-            if f[k] < cost[s]:
-                inc[s], cost[s] = cand[k], f[k]
-                moved = True
-            else:
+            d_tmpl.copy_(torch.from_numpy(inc[s]))
+            plan.eval_gen(N.GEN_NEIGHBOR, 0, 0, M, template=d_tmpl,
+                          group=d_group, n_groups=ng, best=best)
+            b = best.cpu()
+            c = float(b[:1].view(torch.float64).item())
+            idx = int(b[1].item())
+            if idx < 0 or not c < cost[s]:
                 live[s] = False
+                continue
+            if idx < ng * K:
+                j, va, l, vb = idx // K, idx % K, -1, 0
+            else:
+                p = idx - ng * K
+                vb = p % K
+                p //= K
+                va = p % K
+                p //= K
+                l, j = p % ng, p // ng
+                if l <= j:
+                    l = -1
+            inc[s][group == j] = va
+            if l >= 0:
+                inc[s][group == l] = vb
+            cost[s] = c
+            moved = True
         if not moved or (deadline is not None and time.monotonic() > deadline):
             break
     b = int(np.argmin(cost))

@@ -77,3 +77,54 @@ def test_sampled_module_sweep_is_consistent():
     assert _oracle_fit(sdoc, s, 1)[0] == obj
     # never worse than MET on the same module
     assert obj <= hs.met(sub, hw, t, 1).objective
+
+
+def test_neighbor_generation_matches_host():
+    """HS_GEN_NEIGHBOR: every one- and two-group move of an incumbent,
+    generated on the device, equals the host construction, and its
+    makespan the evaluation of that row."""
+    import numpy as np
+    import torch
+    from paper_2308_00127_b200 import _native as N
+    from paper_2308_00127_b200.heuristics import _fit_rows
+    from paper_2308_00127_b200.plan import get_plan
+    g, hw, t = hs.load_instance(instance_doc("ws30"))
+    plan = get_plan(g, hw, t, 1)
+    V, K = plan.V, plan.K
+    rng = np.random.default_rng(4)
+    inc = rng.integers(K, size=V, dtype=np.uint8)
+    group = np.full(V, -1, np.int16)
+    free = [i for i in range(V) if i % 5]  # every fifth position pinned
+    for k, i in enumerate(free):
+        group[i] = min(k, 7 + k // 3)  # some ties
+    # renumber groups by first position (the generator's contract)
+    ren, nxt = {}, 0
+    for i in range(V):
+        if group[i] >= 0:
+            if group[i] not in ren:
+                ren[group[i]] = nxt
+                nxt += 1
+            group[i] = ren[group[i]]
+    ng = nxt
+    M = ng * K + ng * ng * K * K
+    out = torch.empty((M, V), dtype=torch.uint8, device="cuda")
+    ms = torch.empty(M, dtype=torch.float64, device="cuda")
+    plan.eval_gen(N.GEN_NEIGHBOR, 0, 0, M,
+                  template=torch.from_numpy(inc).cuda(),
+                  group=torch.from_numpy(group).cuda(), n_groups=ng,
+                  genes_out=out, makespan=ms)
+    want = np.repeat(inc[None, :], M, axis=0)
+    for c in range(M):
+        if c < ng * K:
+            want[c][group == c // K] = c % K
+        else:
+            p = c - ng * K
+            vb, va = p % K, (p // K) % K
+            p //= K * K
+            l, j = p % ng, p // ng
+            want[c][group == j] = va
+            if l > j:
+                want[c][group == l] = vb
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert np.array_equal(ms.cpu().numpy().view(np.uint64),
+                          _fit_rows(plan, want).view(np.uint64))
