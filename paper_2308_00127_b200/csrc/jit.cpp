@@ -138,6 +138,7 @@ JitOpts JitOpts::from_env() {
             if (k == "tlanes") o.tm_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "tregs") o.tm_regs = std::max(0, std::atoi(v.c_str()));
             if (k == "tdev") o.tm_dev = std::atoi(v.c_str()) != 0;
+            if (k == "blk") o.blk = std::atoi(v.c_str()) != 0;
             // emission-only (hs_plan_emit_specialized): TMEM columns per warp
             // group, normally chosen by jit_build
             if (k == "tcols") o.tm_cols = std::max(0, std::atoi(v.c_str()));
@@ -163,6 +164,57 @@ bool jit_eligible(const Plan &p) {
 
 namespace {
 
+// Link classes of a multi-server platform (the paper's case study,
+// benchgen.gen_transformer_stack): a full mesh whose class of (u, v) is 0
+// on the same device, `ci` between devices of the same node and `co`
+// across nodes, nodes being blocks of B consecutive sorted devices. The
+// class is then (u == v, u / B == v / B) -- a multiply-shift and two
+// compares instead of two table loads per edge. (M, S): d / B == (d * M)
+// >> S for every d < K.
+struct BlockClasses {
+    bool ok = false;
+    int B = 0, ci = 0, co = 0, M = 0, S = 0;
+};
+
+BlockClasses block_classes(const Plan &p) {
+    BlockClasses b;
+    if (p.uniform_comm || !p.full_mesh || p.n_cls != 3 || p.K < 3) return b;
+    const int K = p.K;
+    for (int B = 2; B < K && !b.ok; ++B) {
+        if (K % B) continue;
+        int ci = -1, co = -1;
+        bool ok = true;
+        for (int u = 0; u < K && ok; ++u)
+            for (int v = 0; v < K && ok; ++v) {
+                const size_t at = 2 * (size_t(u) * K + v);  // uint16 little-endian
+                const int c = p.bclass[at] | (p.bclass[at + 1] << 8);
+                if (u == v) {
+                    ok = c == 0;
+                    continue;
+                }
+                int &want = (u / B == v / B) ? ci : co;
+                if (want < 0) want = c;
+                ok = c == want && c != 0 && c != 0xFFFF;
+            }
+        if (ok && ci > 0 && co > 0 && ci != co) {
+            b.B = B;
+            b.ci = ci;
+            b.co = co;
+            for (int S = 6; S < 24 && !b.ok; ++S) {
+                const int M = ((1 << S) + B - 1) / B;
+                bool good = true;
+                for (int d = 0; d < K && good; ++d) good = (d * M) >> S == d / B;
+                if (good) {
+                    b.M = M;
+                    b.S = S;
+                    b.ok = true;
+                }
+            }
+        }
+    }
+    return b;
+}
+
 // Shared-memory layout of the specialised kernel (byte offsets); every
 // table is staged from the plan blob once per CTA.
 struct JitLayout {
@@ -185,7 +237,8 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
         l.durg = true;
     }
     l.avail = o.avail_smem || p.K > 4;
-    l.cls = !p.uniform_comm;
+    // node-block classes need no class tables (computed from the genes)
+    l.cls = !p.uniform_comm && !(o.blk && block_classes(p).ok);
     l.mem = p.mem_check;
     int64_t at = 16;
     if (l.dur) { l.dur_off = at; at += a16(int64_t(p.V) * p.K * 8); }
@@ -408,7 +461,14 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
     // is dropped. Each producer then carries one value f = end + om/beta
     // (one add per producer instead of per edge) and each edge is one
     // predicated compare-and-select: acc = (d_q != d_i && f > acc) ? f : acc.
-    const bool dom = o.dom && !l.cls && !greg;
+    const BlockClasses bk = o.blk && !greg ? block_classes(p) : BlockClasses{};
+    const bool blk = bk.ok && !l.cls;
+    const bool dom = o.dom && !l.cls && !greg && !blk;
+    // both fold "cond|value" terms with the same-device terms dropped
+    const bool domlike = dom || blk;
+    auto node_of = [&](const std::string &d) {
+        return "((" + d + " * " + std::to_string(bk.M) + ") >> " + std::to_string(bk.S) + ")";
+    };
     std::vector<double> prod_c(V, 0.0);
     for (int i = 0; i < V; ++i)
         for (int e = p.nodes[i].e_begin; e < p.nodes[i].e_end; ++e)
@@ -436,6 +496,25 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                 // the producer's f (register name f<q>, or its slot)
                 const std::string fq = in_reg ? "f" + std::to_string(q) : endq;
                 xs.push_back((zero_c(q) ? std::string() : gq + " != " + di) + "|" + fq);
+                continue;
+            }
+            if (blk) {
+                // same device: dominated (dropped); same node: class ci;
+                // other node: class co (om / beta of either, constant memory)
+                const std::string nq = (near > 0 && i - q <= near)
+                                           ? "n" + std::to_string(q) : node_of(gq);
+                const double cin = p.ctab[size_t(q) * p.n_cls + bk.ci];
+                const double cout = p.ctab[size_t(q) * p.n_cls + bk.co];
+                std::string ci_s = lit(cin), co_s = lit(cout);
+                if (std::isfinite(cin) && std::isfinite(cout)) {
+                    ci_s = "HSC[" + std::to_string(cconst.size()) + "]";
+                    cconst.push_back(cin);
+                    co_s = "HSC[" + std::to_string(cconst.size()) + "]";
+                    cconst.push_back(cout);
+                }
+                s += "    const double " + x + " = " + endq + " + dsel(" + nq + " == n" + is +
+                     ", " + ci_s + ", " + co_s + ");\n";
+                xs.push_back(gq + " != " + di + "|" + x);
                 continue;
             }
             if (l.cls) {
@@ -586,6 +665,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
         }
         if (greg && !preds[i].empty())
             s += "    const hs_u32 DP" + is + " = (hs_u32)" + di + " * 0x55555555u;\n";
+        if (blk) s += "    const int n" + is + " = " + node_of(di) + ";\n";
         if (l.cls) s += "    int nl" + is + " = 0;\n";
         if (o.tmem) tm_loads(i);
         // early terms: predecessors placed at or before i - D - 1 (in edge
@@ -597,7 +677,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                 xs.push_back(t[0]);
             }
         if (!xs.empty())
-            early[i] = dom ? fold(xs, "re" + is, "0.0") : max_tree(xs, is + "e");
+            early[i] = domlike ? fold(xs, "re" + is, "0.0") : max_tree(xs, is + "e");
     };
     auto tail = [&](int i) {
         const std::string is = std::to_string(i), di = "d" + is;
@@ -622,7 +702,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
                 auto t = edge_terms(i, int(k), int(k) + 1);
                 xs.push_back(t[0]);
             }
-        if (!early[i].empty() && !dom) xs.push_back(early[i]);
+        if (!early[i].empty() && !domlike) xs.push_back(early[i]);
         if (l.cls) s += "    st = first_status(st, nl" + is + ", ST_LINK);\n";
         if (!p.latency_complete) {
             uint64_t miss = 0;
@@ -636,7 +716,7 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
             }
         }
         const std::string r = "r" + is;
-        if (dom)
+        if (domlike)
             fold(xs, r, early[i].empty() ? "0.0" : early[i]);
         else if (xs.empty())
             s += "    const double " + r + " = 0.0;\n";

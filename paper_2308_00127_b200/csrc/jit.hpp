@@ -42,6 +42,8 @@ struct JitOpts {
                               // measured neutral on WS200, -3 % on the WS
                               // 10x20 stack (profiles r2e), so off
     int gslot_lanes = 192;    // lanes per CTA with global-memory slots (sweep r1h)
+    bool blk = true;          // node-block link classes computed, not looked up
+                              // (full mesh; same device / same node / other)
     static JitOpts from_env();
 };
 
