@@ -143,7 +143,10 @@ JitOpts JitOpts::from_env() {
             // group, normally chosen by jit_build
             if (k == "tcols") o.tm_cols = std::max(0, std::atoi(v.c_str()));
             if (k == "dsmem") o.dur_smem_max = std::atoi(v.c_str());
-            if (k == "lanes") o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
+            if (k == "lanes") {
+                o.lanes = std::max(32, std::min(1024, std::atoi(v.c_str())));
+                o.lanes_set = true;
+            }
         }
         at = end + 1;
     }
@@ -998,9 +1001,14 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     const int64_t budget = int64_t(optin) - head - 1024;
     JitOpts ob = o;  // slots in shared memory
     ob.tmem = false;
+    // no end-time slots and the device state in shared memory (K > 4, the
+    // multi-server platforms): 12 warps like the TMEM tier (tf96 +11 %,
+    // profiles r2o); otherwise `lanes`
+    const int cap_lanes = slots == 0 && p.K > kMaxRegK && !o.lanes_set
+                              ? std::max(o.lanes, o.tm_lanes) : o.lanes;
     auto lanes_for = [&](bool db) {
         return int(std::min<int64_t>(budget / per_lane_bytes(p, ob, slots, ld_cap, db),
-                                     o.lanes) / 32 * 32);
+                                     cap_lanes) / 32 * 32);
     };
     // double-buffer the genome tile only when it costs no lanes
     bool dbuf = lanes_for(true) >= lanes_for(false);

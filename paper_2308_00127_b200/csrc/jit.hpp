@@ -24,6 +24,7 @@ struct JitOpts {
     int near = 8;             // > 0: split residency (registers for consumers
                               // within `near` positions, long storage beyond)
     int lanes = 256;          // threads (= candidates) per CTA, at most
+    bool lanes_set = false;   // `lanes` given explicitly (HS_JIT_OPTS)
     int ahead = 2;            // software pipelining distance (tasks)
     bool dom = true;          // drop same-device predecessor terms (dominated)
     bool gword = false;       // genes read four per 32-bit shared-memory load
