@@ -141,3 +141,36 @@ def test_ea_draw_matches_host_stream():
                 a, b = moff[c, k], moff[c, k + 1]
                 assert [(int(x), int(y)) for x, y in
                         zip(mpos[a:b], mval[a:b])] == m, (V, c, k)
+
+
+def test_multi_edge_cases():
+    """budget 0, one device, empty seed list, a single seed, and the
+    reference's small golden instances (tight memory, missing links, L > 1)
+    through the multi-chain paths: each element equals the single run."""
+    from conftest import golden
+    from paper_2308_00127_b200.core import load_graph, load_hardware, \
+        load_latency
+    import json
+    assert hs.simulated_annealing_multi(*hs.load_instance(
+        instance_doc("ws30")), 1, []) == []
+    for e in golden("heuristics")[:8] + golden("heuristics")[-2:]:
+        g = load_graph(json.dumps(e["graph"]))
+        hw = load_hardware(json.dumps(e["hardware"]))
+        t = load_latency(json.dumps(e["latency"]))
+        L = e["L"]
+        for budget in (0, 1, 150):
+            for multi, single in (
+                    (hs.simulated_annealing_multi, hs.simulated_annealing),
+                    (hs.one_plus_one_ea_multi, hs.one_plus_one_ea)):
+                try:
+                    want = [single(g, hw, t, L, seed=s, budget=budget)
+                            for s in (0, 1, 2)]
+                except hs.ScheduleError:
+                    with pytest.raises(hs.ScheduleError):
+                        multi(g, hw, t, L, [0, 1, 2], budget=budget)
+                    continue
+                got = multi(g, hw, t, L, [0, 1, 2], budget=budget)
+                assert [fhex(s.objective) for s in got] == \
+                    [fhex(s.objective) for s in want], (e["name"], budget)
+                assert [_mapping(s) for s in got] == \
+                    [_mapping(s) for s in want]
