@@ -459,9 +459,10 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.window = std::min(window, a.lanes);
     Scratch spec;
     spec.s = stream;
-    // speculation scratch, one window per chain: [fit f64 | pos i32 | new
-    // u8 | status u8] x (chains * window)
-    const size_t nw = size_t(e.window) * size_t(chains);
+    // speculation scratch per chain: window base steps + 32 continuation
+    // steps (two-level): [fit f64 | pos i32 | new u8 | status u8]
+    e.spec_stride = int64_t(e.window) + 32;
+    const size_t nw = size_t(e.spec_stride) * size_t(chains);
     CK(cudaMallocAsync(&spec.ptr, nw * 16 + 64, stream));
     uint8_t *sp = static_cast<uint8_t *>(spec.ptr);
     e.sfit = reinterpret_cast<double *>(sp);
@@ -480,6 +481,9 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     e.budget = budget;
     const char *hx = getenv("HS_SA_HOST_EXP");
     e.host_exp = hx && atoi(hx) ? 1 : 0;
+    // second level: continuation steps per branch (0 = off; HS_SA_LEVEL2)
+    const char *lv = getenv("HS_SA_LEVEL2");
+    e.two_level = lv ? std::max(0, std::min(16, atoi(lv))) : 8;
     rc = jm ? hs::jit_launch_search(*jm, 1, a, &e, stream, &err, chains)
             : hs::launch_sa(*ds, !plan->p.uniform_comm, a, e, stream, &err, chains);
     if (rc) return set_err(rc, err);

@@ -145,8 +145,12 @@ struct SaParams {
     int host_exp;      // test hook: hand every Metropolis test to the host
     // independent chains (hs_sa_run_multi): CTA c runs chain c with genes /
     // best at + c * chain_stride, rng + 4c, buf + 2c, f + 8c, istate + 8c and
-    // its own speculation scratch (+ c * window); 0 = one chain
+    // its own speculation scratch (+ c * spec_stride); 0 = one chain
     hs_i64 chain_stride;
+    // speculation scratch entries per chain: window (base steps) + 32 (the
+    // second level's continuation warp: two branches of 16)
+    hs_i64 spec_stride;
+    int two_level;     // second level: continuation steps per branch (0: off)
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
@@ -672,21 +676,32 @@ struct Pcg64 {
 };
 
 // K10 driver: simulated annealing (heuristics.py:259-299) in one launch of
-// a single CTA. Rounds of speculation: thread 0 draws the next k steps'
-// moves assuming each is rejected after a random() draw (a finite, worse
-// candidate -- the only way a step continues a round); the lanes evaluate
-// those k candidates against the current genome; thread 0 then replays the
-// steps with the real generator and ends the round at the first acceptance
-// or infinite candidate (where the speculated draws diverge). Metropolis
-// needs exp(): when u lies within a few ulp of the device exp the step is
-// handed back to the host (CPython's math.exp decides; never observed in
-// practice), so the trajectory is the reference's exactly. Shared by the
-// AOT kernel (kernels.cu) and the specialised module (jit.cpp).
+// a single CTA per chain. Rounds of speculation: thread 0 draws the next k
+// steps' moves assuming each is rejected after a random() draw (a finite,
+// worse candidate -- the only way a step continues a round); the lanes
+// evaluate those k candidates against the current genome; thread 0 then
+// replays the steps with the real generator and ends the round at the first
+// acceptance or infinite candidate (where the speculated draws diverge).
+// Second level (e.two_level steps, when one more warp fits): the commonest
+// round ends with step 0 accepted, so one extra warp evaluates further
+// steps on top of step 0's move for each way step 0 can be accepted
+// (delta <= 0: no random() drawn; delta > 0 and the Metropolis test passed:
+// random() drawn) -- lanes 0-15 and 16-31 --, their moves drawn by threads
+// 32 and 64 from the two generator states while thread 0 draws the base
+// steps; such a round goes on into the matching branch and can make two
+// acceptances. Metropolis needs exp():
+// when u lies within a few ulp of the device exp the step is handed back to
+// the host (CPython's math.exp decides; never observed in practice), so the
+// trajectory is the reference's exactly. Shared by the AOT kernel
+// (kernels.cu) and the specialised module (jit.cpp).
 template <class Body>
 __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0, hs_u8 *smem,
                                          Body &body) {
-    __shared__ int s_k, s_step, s_go, s_apos;
+    __shared__ int s_k, s_step, s_go, s_apos, s_apos2, s_pos0, s_new0;
+    __shared__ hs_u64 s_q[2][4];  // branch starts: after step 0's draws (A), + random() (B)
+    __shared__ hs_u32 s_qb[2][2];
     SaParams e = e0;  // this CTA's chain
+    const hs_i64 sp = e0.spec_stride;
     if (e0.chain_stride) {
         const hs_i64 c = blockIdx.x;
         e.genes += c * e0.chain_stride;
@@ -695,23 +710,24 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
         e.buf += 2 * c;
         e.f += 8 * c;
         e.istate += 8 * c;
-        e.spos += c * e0.window;
-        e.snew += c * e0.window;
-        e.sfit += c * e0.window;
-        e.sst += c * e0.window;
+        e.spos += c * sp;
+        e.snew += c * sp;
+        e.sfit += c * sp;
+        e.sst += c * sp;
     }
     const int l = threadIdx.x;
     hs_u8 *row = smem + a.smem_tile + (hs_i64)l * a.ld_s;
     hs_u8 *genes = e.genes;
     // a lane's row stays the current genome between rounds: it undoes its
-    // own move and takes the round's accepted move (s_apos) instead of
-    // re-copying V bytes; a lane that sat a round out copies in full
-    int prev = -1;
+    // own move(s) and takes the round's accepted moves (s_apos, s_apos2)
+    // instead of re-copying V bytes; a lane that sat a round out copies in
+    // full
+    int prev = -1, prev0 = -1;
     bool synced = false;
     // the row's bytes past V stay 0 (the specialised body may read whole
     // words of the row and rely on every byte being a valid gene)
     for (int i = a.V; i < a.ld_s; ++i) row[i] = 0;
-    const int V = a.V, budget = e.budget;
+    const int V = a.V, budget = e.budget, W = e.window;
     const hs_u32 nd1 = (hs_u32)(e.n_dev - 1);
     Pcg64 r;
     double cur = 0.0, bestf = 0.0, temp = 0.0;
@@ -730,81 +746,142 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
         step = e.istate[0];
         // the first round's window comes from the caller: at most the
         // scratch arrays' length (e.window <= lanes)
-        s_k = e.istate[1] < 1 ? 1 : (e.istate[1] < e.window ? e.istate[1] : e.window);
+        s_k = e.istate[1] < 1 ? 1 : (e.istate[1] < W ? e.istate[1] : W);
         s_step = step;
         s_go = 1;
-        s_apos = -1;
+        s_apos = s_apos2 = -1;
     }
     __syncthreads();
+    auto draw_move = [&](Pcg64 &q, int &pos, int &nw, int pos0, int new0) {
+        pos = q.integers((hs_u32)V);
+        const int old = pos == pos0 ? new0 : genes[pos];
+        nw = old;
+        if (e.n_dev > 1) {
+            nw = q.integers(nd1);
+            if (nw >= old) ++nw;
+        }
+    };
     for (;;) {
         const int kk = s_k, stp = s_step;
         if (!s_go || stp >= budget) break;
         const int n = kk < budget - stp ? kk : budget - stp;
+        const int wb = (n + 31) & ~31;  // first lane after the base warps
+        // one more warp: branch A in its lanes 0..15, branch B in 16..31,
+        // e.two_level continuation steps each (at most 16)
+        const bool lvl2 = e.two_level > 0 && e.n_dev > 1 && wb + 32 <= a.lanes &&
+                          budget - stp > 1;
+        const int m2 = e.two_level < 16 ? e.two_level : 16;
+        const int m = lvl2 ? (m2 < budget - stp - 1 ? m2 : budget - stp - 1) : 0;
         if (l == 0) {  // speculative moves of the next n steps
             Pcg64 q = r;
-            for (int i = 0; i < n; ++i) {
-                const int pos = q.integers((hs_u32)V);
-                const int old = genes[pos];
-                int nw = old;
-                if (e.n_dev > 1) {
-                    nw = q.integers(nd1);
-                    if (nw >= old) ++nw;
-                }
+            int pos, nw;
+            draw_move(q, pos, nw, -1, 0);
+            e.spos[0] = pos;
+            e.snew[0] = (hs_u8)nw;
+            if (lvl2) {
+                s_pos0 = pos;
+                s_new0 = nw;
+                s_q[0][0] = q.slo, s_q[0][1] = q.shi, s_qb[0][0] = q.has, s_qb[0][1] = q.cached;
+            }
+            (void)q.random();
+            if (lvl2) s_q[1][0] = q.slo, s_q[1][1] = q.shi, s_qb[1][0] = q.has, s_qb[1][1] = q.cached;
+            __threadfence_block();
+            if (lvl2) atomicExch(&s_go, 2);  // branch starts published
+            for (int i = 1; i < n; ++i) {
+                draw_move(q, pos, nw, -1, 0);
                 e.spos[i] = pos;
                 e.snew[i] = (hs_u8)nw;
                 (void)q.random();
             }
+        } else if (lvl2 && (l == 32 || l == 64)) {
+            // the two continuation streams, drawn by warps 1 and 2 while
+            // thread 0 draws the base steps
+            const int b = l == 32 ? 0 : 1;
+            while (atomicAdd(&s_go, 0) != 2) {
+            }
+            __threadfence_block();
+            Pcg64 q;
+            q.slo = s_q[b][0];
+            q.shi = s_q[b][1];
+            q.ilo = e.rng[2];
+            q.ihi = e.rng[3];
+            q.has = s_qb[b][0];
+            q.cached = s_qb[b][1];
+            const int p0 = s_pos0, n0 = s_new0;
+            for (int j = 0; j < m; ++j) {
+                int pos, nw;
+                draw_move(q, pos, nw, p0, n0);
+                e.spos[W + 16 * b + j] = pos;
+                e.snew[W + 16 * b + j] = (hs_u8)nw;
+                (void)q.random();
+            }
         }
         __syncthreads();
-        const bool valid = l < n;
-        if ((l & ~31) < n) {  // warp-uniform: warps past the window sit out
+        if (l == 0 && lvl2) s_go = 1;
+        const int w0 = l & ~31;
+        const bool active = w0 < wb || (lvl2 && w0 == wb);
+        if (active) {  // warp-uniform: warps past the window sit out
             if (synced) {
+                if (prev0 >= 0) row[prev0] = genes[prev0];
                 if (prev >= 0) row[prev] = genes[prev];
-                const int ap = s_apos;
+                const int ap = s_apos, ap2 = s_apos2;
                 if (ap >= 0) row[ap] = genes[ap];
+                if (ap2 >= 0) row[ap2] = genes[ap2];
             } else {
                 for (int i = 0; i < V; ++i) row[i] = genes[i];
                 synced = true;
             }
-            prev = -1;
+            prev = prev0 = -1;
+            int slot;
+            bool valid;
+            if (w0 < wb) {
+                slot = l;
+                valid = l < n;
+            } else {
+                const int b = (l - wb) >> 4, j = (l - wb) & 15;
+                slot = W + 16 * b + j;
+                valid = j < m;
+                prev0 = e.spos[0];
+                row[prev0] = e.snew[0];  // on top of step 0's move
+            }
             if (valid) {
-                prev = e.spos[l];
-                row[prev] = e.snew[l];
+                prev = e.spos[slot];
+                row[prev] = e.snew[slot];
             }
             double ms = 0.0;
             int st = 0;
-            body.run(row, l, stp + l, valid, 0, ms, st);
+            body.run(row, l, stp + slot, valid, 0, ms, st);
             if (valid) {
-                e.sfit[l] = ms;
-                e.sst[l] = (hs_u8)st;
+                e.sfit[slot] = ms;
+                e.sst[slot] = (hs_u8)st;
             }
         } else {
             synced = false;
         }
         __syncthreads();
         if (l == 0) {  // replay with the real generator
-            bool acc = false;
+            bool acc = false, acc0 = false, mh0 = false;
+            int i = 0;
             ++rounds;
-            s_apos = -1;
-            for (int i = 0; i < n; ++i) {
-                const int pos = r.integers((hs_u32)V);
-                const int old = genes[pos];
-                int nw = old;
-                if (e.n_dev > 1) {
-                    nw = r.integers(nd1);
-                    if (nw >= old) ++nw;
-                }
-                const double cand = e.sfit[i];
-                if (e.sst[i] >= ST_MISSING) {  // fitness raised
+            s_apos = s_apos2 = -1;
+            // one step at scratch slot `slot` (kind: 0 base, 1 continuation);
+            // returns true when the round ends here
+            auto replay = [&](int slot, int kind) -> bool {
+                int pos, nw;
+                draw_move(r, pos, nw, -1, 0);
+                const double cand = e.sfit[slot];
+                if (e.sst[slot] >= ST_MISSING) {  // fitness raised
                     stop = 2;
-                    e.istate[3] = e.sst[i];
-                    break;
+                    e.istate[3] = e.sst[slot];
+                    return true;
                 }
                 const double delta = cand - cur;
                 acc = delta <= 0.0;
                 const bool fin = isfinite(cand);
+                bool drew = false;
                 if (!acc && fin) {
                     const double u = r.random();
+                    drew = true;
                     const double ex = exp(-delta / temp);
                     // temp == 0 (cooled to underflow): the reference's
                     // -delta / temp raises ZeroDivisionError -- the host's
@@ -816,14 +893,14 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
                         e.istate[5] = nw;
                         e.f[3] = cand;
                         e.f[4] = u;
-                        break;
+                        return true;
                     }
                     acc = u < ex;
                 }
                 ++step;
                 if (acc) {
                     genes[pos] = (hs_u8)nw;
-                    s_apos = pos;
+                    if (kind == 0) s_apos = pos; else s_apos2 = pos;
                     cur = cand;
                     if (cand < bestf) {
                         bestf = cand;
@@ -831,9 +908,22 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
                     }
                 }
                 temp *= e.alpha;
-                if (acc || !fin) break;
+                if (kind == 0 && slot == 0) {
+                    acc0 = acc;
+                    mh0 = drew;
+                }
+                return acc || !fin;
+            };
+            for (i = 0; i < n; ++i)
+                if (replay(i, 0)) break;
+            // step 0 accepted: the round goes on into the matching branch
+            if (lvl2 && !stop && acc0 && i == 0) {
+                acc = false;
+                const int base = W + (mh0 ? 16 : 0);
+                for (int j = 0; j < m && step < budget; ++j)
+                    if (replay(base + j, 1)) break;
             }
-            s_k = acc ? 8 : (2 * kk < e.window ? 2 * kk : e.window);
+            s_k = acc ? 8 : (2 * kk < W ? 2 * kk : W);
             s_step = step;
             if (stop) s_go = 0;
         }
