@@ -146,8 +146,11 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
     }
     // plan tables in shared memory unless that costs more than one warp
     ds->plan_smem = la >= 32 && la >= lb - 32;
-    ds->T = ds->plan_smem ? la : lb;
-    if (ds->T >= 32) {
+    auto configure = [&](bool psm) {
+        ds->plan_smem = psm;
+        ds->T = psm ? la : lb;
+        ds->blocks_per_sm = 0;
+        if (ds->T < 32) return;
         ds->lanes = ds->T;
         ds->smem_tile = 16 + (ds->plan_smem ? p.lay.eval_bytes : 0);
         ds->smem_ends = ds->smem_tile +
@@ -160,6 +163,16 @@ int get_dev_state(const Plan &p, const DevState **out, std::string *err) {
                                   : eval_occupancy(ds->kt, cls, ds->T, ds->smem, &blocks);
         if (orc != HS_OK) blocks = 0;
         ds->blocks_per_sm = blocks;
+    };
+    configure(ds->plan_smem);
+    // the batched-variant kernel is latency-bound at one CTA per SM (ncu
+    // r2w: 12.5 % occupancy, 7 cycles per issue): when its tables read
+    // through L1 leave room for more resident lanes (several CTAs per SM),
+    // take that configuration
+    if (p.batched && ds->plan_smem) {
+        const int64_t with = int64_t(ds->T) * ds->blocks_per_sm;
+        configure(false);
+        if (int64_t(ds->T) * ds->blocks_per_sm <= with) configure(true);
     }
     if (ds->blocks_per_sm < 1) {  // eval unusable; bounds kernels still run
         ds->T = ds->lanes = 0;

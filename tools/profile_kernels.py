@@ -6,6 +6,7 @@
     sa_multi   148 SA chains, WS 10x20 (hs_jit_sa, grid 148)
     ea_multi   148 EA chains, WS 10x20 (ea_draw_kernel, hs_jit_ea)
     validate   K11 over 2,000 decoded WS200 schedules
+    batched    K8 (batched variant) on fused ResNet-50, L = 4
 """
 import json
 import os
@@ -61,3 +62,13 @@ elif what == "validate":
         hs.validate_schedules(g, hw, t, scheds)
 torch.cuda.synchronize()
 print("done", what)
+if what == "batched":
+    # K8 on fused ResNet-50 at L = 4 (15 options, 3 parts)
+    g, hw, t = load("rn50f")
+    opts = hs.batched_options(g, hw, t, 4)
+    genes = torch.randint(0, len(opts), (1 << 22, 112), dtype=torch.uint8,
+                          device="cuda")
+    for _ in range(3):
+        hs.fitness_batched(genes, g, hw, t, 4)
+    torch.cuda.synchronize()
+    print("done batched")
