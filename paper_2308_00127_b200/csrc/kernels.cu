@@ -188,8 +188,87 @@ struct BatchedBody {
     int lanes, V, K, n_opt, P, ncls;
     bool nan;
 
+    // P <= PM parts per option (PM = 2 or 4; every L <= 8 with the default
+    // sub-batch sizes): each predecessor's option and parts are loaded once per edge
+    // and every own part is relaxed from them (per-part maxima in
+    // registers, the same order of max operations per part as below)
+    template <int PM>
+    __device__ __forceinline__ void runp(const hs_u8 *grow, int li, hs_i64 cand,
+                                         bool valid, double &ms_out, int &st_out) {
+        double *ecol = ends + li;
+        double *av = kstate + li;
+        for (int k = 0; k < K; ++k) av[k * lanes] = 0.0;
+        double ms = 0.0;
+        int st = 0, bad = 0;
+        for (int i = 0; i < V; ++i) {
+            const NodeRec nr = nodes[i];
+            int o = grow[i];
+            bad |= o >= n_opt;
+            o = o < n_opt ? o : 0;
+            const int np = bnp[o];
+            int dk[PM], lok[PM], hik[PM], nl[PM];
+            double r[PM];
+#pragma unroll
+            for (int k = 0; k < PM; ++k) {
+                const int *q = bopt + (o * P + (k < np ? k : 0)) * 4;
+                dk[k] = q[0];
+                lok[k] = q[1];
+                hik[k] = q[2];
+                r[k] = 0.0;
+                nl[k] = 0;
+            }
+            for (int e = nr.e_begin; e < nr.e_end; ++e) {
+                const EdgeRec er = edges[e];
+                int op = grow[er.gpos];
+                op = op < n_opt ? op : 0;
+                const int npp = bnp[op];
+                for (int m = 0; m < npp; ++m) {
+                    const int *qq = bopt + (op * P + m) * 4;
+                    const int dm = qq[0], lom = qq[1], him = qq[2];
+                    const double em = ecol[(er.slot * P + m) * lanes];
+#pragma unroll
+                    for (int k = 0; k < PM; ++k) {
+                        if (k >= np || him < lok[k] || lom > hik[k]) continue;
+                        int cls = bclass[dm * K + dk[k]];
+                        if (cls == 0xFFFF) {
+                            nl[k] = 1;
+                            cls = 0;
+                        }
+                        r[k] = pymax(r[k], em + ctab[er.crow + cls]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PM; ++k) {
+                if (k >= np) continue;
+                const int d = dk[k];
+                if (nl[k] && !st) st = ST_LINK;
+                const hs_i64 at = ((hs_i64)i * n_opt + o) * P + k;
+                if (!bdur_ok[at] && !st) st = ST_MISSING;
+                const double s = pymax(r[k], av[d * lanes]);
+                const double e = s + bdur[at];
+                if (starts && valid) starts[(cand * V + i) * P + k] = s;
+                if (nr.out_slot >= 0) ecol[(nr.out_slot * P + k) * lanes] = e;
+                av[d * lanes] = e;
+                ms = pymax(ms, e);
+            }
+        }
+        if (bad) st = ST_GENE;
+        if (st) ms = st >= ST_MISSING ? knan() : kinf();
+        ms_out = ms;
+        st_out = st;
+    }
+
     __device__ __forceinline__ void run(const hs_u8 *grow, int li, hs_i64 cand,
                                         bool valid, int, double &ms_out, int &st_out) {
+        if (P <= 2) {
+            runp<2>(grow, li, cand, valid, ms_out, st_out);
+            return;
+        }
+        if (P <= 4) {
+            runp<4>(grow, li, cand, valid, ms_out, st_out);
+            return;
+        }
         double *ecol = ends + li;
         double *av = kstate + li;
         for (int k = 0; k < K; ++k) av[k * lanes] = 0.0;
