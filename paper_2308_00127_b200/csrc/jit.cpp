@@ -138,6 +138,7 @@ JitOpts JitOpts::from_env() {
             if (k == "tlanes") o.tm_lanes = std::max(32, std::atoi(v.c_str()));
             if (k == "tregs") o.tm_regs = std::max(0, std::atoi(v.c_str()));
             if (k == "tdev") o.tm_dev = std::atoi(v.c_str()) != 0;
+            if (k == "tctas") o.tm_ctas = std::atoi(v.c_str()) >= 2 ? 2 : 1;
             if (k == "blk") o.blk = std::atoi(v.c_str()) != 0;
             // emission-only (hs_plan_emit_specialized): TMEM columns per warp
             // group, normally chosen by jit_build
@@ -860,11 +861,13 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
          "  body.tb = 0u;\n"
          "  body.dg = reinterpret_cast<const double *>(a.blob + a.lay.dur);\n";
     if (o.tmem) {
-        // the whole TMEM of the SM (one CTA per SM): warp 0 allocates 512
-        // columns; each warp uses its lane quadrant and a column band
+        // the TMEM of the SM (512 columns, or its share with tm_ctas CTAs
+        // per SM): warp 0 allocates; each warp uses its lane quadrant and a
+        // column band
+        const std::string ncols = std::to_string(512 / std::max(1, o.tm_ctas));
         s += "  __shared__ hs_u32 tm_base_s;\n"
              "  if (threadIdx.x < 32) {\n"
-             "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" "
+             "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], " + ncols + ";\" "
              ":: \"r\"(smem_addr(&tm_base_s)) : \"memory\");\n"
              "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\" ::: \"memory\");\n"
              "  }\n"
@@ -882,16 +885,18 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
              "  __syncthreads();\n"
              "  if (threadIdx.x < 32) {\n"
              "    asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
-             "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" "
+             "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, " +
+             std::to_string(512 / std::max(1, o.tm_ctas)) + ";\" "
              ":: \"r\"(tm_base_s) : \"memory\");\n"
              "  }\n";
     s += "}\n";
+    const int min_blocks = o.tmem ? std::max(1, o.tm_ctas) : 1;
     std::snprintf(buf, sizeof buf,
-                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "extern \"C\" __global__ void __launch_bounds__(%d, %d) "
                   "hs_jit_eval(const EvalParams a) { jit_main<false, 0>(a, nullptr, nullptr); }\n"
-                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "extern \"C\" __global__ void __launch_bounds__(%d, %d) "
                   "hs_jit_trace(const EvalParams a) { jit_main<true, 0>(a, nullptr, nullptr); }\n",
-                  T, T);
+                  T, min_blocks, T, min_blocks);
     s += buf;
     if (jit_search_ok(p) && o.sync == 0) {
         // single-CTA search drivers (SA K10, EA K9) over the specialised body
@@ -1038,18 +1043,24 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     int n_slots = slots;
     if (o.tmem && !oe.gslots && slots > 0) {
         JitOpts ot = o;
-        ot.lanes = o.tm_lanes;
+        ot.lanes = o.tm_lanes / o.tm_ctas;
         ot.reg_budget = o.tm_regs;
         const int slots_t = jit_emit(p, 32, ot, nullptr);
+        // several CTAs per SM share its shared memory and its 512 columns
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const int64_t budget_t = o.tm_ctas > 1
+            ? std::min<int64_t>(budget, int64_t(smem_sm) / o.tm_ctas - 1024 - head - 1024)
+            : budget;
         auto lanes_t = [&](bool db) {
-            return int(std::min<int64_t>(budget / per_lane_bytes(p, ot, slots_t, ld_cap, db),
+            return int(std::min<int64_t>(budget_t / per_lane_bytes(p, ot, slots_t, ld_cap, db),
                                          ot.lanes) / 32 * 32);
         };
         const bool dt = lanes_t(true) >= lanes_t(false);
         const int Tt = std::min(lanes_t(dt), 512);
         const int groups = (Tt / 32 + 3) / 4;
         // column bands 4-aligned (the .x4 slot accesses start on them)
-        const int cols = groups > 0 ? (512 / groups) & ~3 : 0;
+        const int cols = groups > 0 ? (512 / o.tm_ctas / groups) & ~3 : 0;
         if (Tt >= 32 && slots_t > 0 && (ot.tm_dev ? 4 : 2) * slots_t > cols)
             ot.tm_dev = false;  // the device column does not fit: end times only
         if (Tt >= 32 && slots_t > 0 && 2 * slots_t <= cols) {
@@ -1175,7 +1186,8 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     m->blocks_per_sm = std::max(1, std::min(2048 / T, int(smem_sm / (m->smem + 1024))));
-    if (m->tmem) m->blocks_per_sm = 1;  // each CTA allocates all 512 TMEM columns
+    // each CTA allocates 512 / tm_ctas TMEM columns
+    if (m->tmem) m->blocks_per_sm = std::min(m->blocks_per_sm, oe.tm_ctas);
     m->sms = sms;
     m->src_bytes = src.size();
     m->compile_ms = std::chrono::duration<double, std::milli>(

@@ -37,6 +37,8 @@ struct JitOpts {
     int tm_lanes = 384;       // lanes per CTA with TMEM slots (12 warps)
     int tm_regs = 40;         // long-lived end times in registers with TMEM slots
     int tm_cols = 0;          // (set by jit_build) TMEM columns per warp group
+    int tm_ctas = 1;          // CTAs per SM on the TMEM tier (each allocates
+                              // 512 / tm_ctas columns, lanes / tm_ctas lanes)
     bool tm_dev = false;      // TMEM slots also hold the producer's device
                               // (4 columns per slot: the consumer's device
                               // compare needs no shared-memory gene load);
