@@ -40,6 +40,7 @@ def fitness_batched(genes, g, hw, table, L: int, *,
     CUDA tensor -> device path)."""
     plan = _plan(g, hw, table, L, splits)
     genes = _batch_genes(genes, plan.V)
+    plan.maybe_specialize(len(genes))  # graph-specialised K8 for big batches
     if hasattr(genes, "data_ptr"):
         import torch
         n = genes.shape[0]
@@ -126,6 +127,7 @@ def random_search_batched(g, hw, table, L: int, n: int, *, seed: int = 0,
     (makespan, index, genes)."""
     import torch
     plan = _plan(g, hw, table, L, splits)
+    plan.maybe_specialize(n)
     best = torch.empty(2, dtype=torch.int64, device="cuda")
     plan.eval_gen(N.GEN_RANDOM, seed, 0, n, best=best)
     b = best.cpu()

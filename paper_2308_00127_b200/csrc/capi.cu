@@ -265,7 +265,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
                                   "evaluator (live end-time slots of one warp "
                                   "exceed the per-CTA shared memory)");
 
-    const hs::JitModule *jm = p.batched ? nullptr : hs::find_jit(p, ds->device);
+    const hs::JitModule *jm = hs::find_jit(p, ds->device);
     Scratch repack;
     repack.s = stream;
     // the specialised kernel reads its staged rows as 32-bit words
@@ -595,7 +595,10 @@ int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
     if (!hs::jit_eligible(plan->p))
         return set_err(HS_EINVAL, "plan not eligible for the specialised evaluator");
     std::string src;
-    hs::jit_emit(plan->p, lanes, hs::JitOpts::from_env(), &src);
+    if (plan->p.batched)
+        hs::jit_emit_batched(plan->p, lanes, hs::JitOpts::from_env(), &src, true);
+    else
+        hs::jit_emit(plan->p, lanes, hs::JitOpts::from_env(), &src);
     if (len) *len = int64_t(src.size());
     if (buf && cap > 0) {
         const size_t m = std::min<size_t>(src.size(), size_t(cap - 1));

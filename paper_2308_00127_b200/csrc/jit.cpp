@@ -161,9 +161,12 @@ static int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 // kernel.
 constexpr int kJitMaxV = 1100, kJitMaxE = 2600, kJitMaxK = 64;
 
+bool jit_batched_ok(const Plan &p);
+
 bool jit_eligible(const Plan &p) {
-    return !p.batched && p.K <= kJitMaxK && !p.nan_possible && p.V > 0 &&
-           p.V <= kJitMaxV && p.E <= kJitMaxE;
+    if (p.batched) return jit_batched_ok(p);
+    return p.K <= kJitMaxK && !p.nan_possible && p.V > 0 && p.V <= kJitMaxV &&
+           p.E <= kJitMaxE;
 }
 
 namespace {
@@ -268,12 +271,19 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
 
 int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap,
                        bool dbuf) {
+    if (p.batched)  // tiles, [slot][part] end times, device-available times
+        return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 * p.P + 8 * p.K;
     const bool avail = o.avail_smem || p.K > 4;
     if (o.gslots || o.tmem) slots = 0;
     return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
 }
 
 int64_t head_bytes(const Plan &p, const JitOpts &o) {
+    if (p.batched) {  // bat_layout's tables
+        const int64_t NO = p.n_opt, VNP = int64_t(p.V) * p.n_opt * p.P;
+        return 16 + a16(NO * NO * 2) + a16(NO * 8) + a16(VNP * 8) +
+               (p.latency_complete ? 0 : a16(VNP));
+    }
     return jit_layout(p, o, 32, 0, 0).head;
 }
 
@@ -288,6 +298,260 @@ std::string stage(int64_t dst, const char *section, int64_t bytes) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Batched-variant plans (K8's semantics, heuristics.py:363-433): the gene is
+// an option (a decomposition of L over distinct devices) and each task has
+// up to P parts. Straight-line code per task like K1', with the option
+// structure folded into two small shared-memory tables built here:
+//   OPT[o]      part k of option o: device in bits 16k..16k+7, "part
+//               exists" in bit 16k+8;
+//   OVD[oq][oi] bit 4m+k set when part m of the producer's option oq and
+//               part k of the consumer's option oi both exist, hold a common
+//               input (the reference's per-input ready time) and sit on
+//               different devices -- a same-device term is dominated by
+//               the device's available time (no NaN), as in K1'.
+// Each term is then one bit test folded into the predicated max. Uniform
+// full-mesh bandwidth only (one om/beta per producer); the parts' end times
+// live in registers for consumers within `near` positions, else in
+// shared-memory slots [slot][part][lane].
+bool jit_batched_ok(const Plan &p) {
+    if (!(p.batched && p.P <= 4 && p.n_opt <= 255 && p.full_mesh && p.n_classes <= 1 &&
+          p.K <= kJitMaxK && !p.nan_possible && p.V > 0 && p.V <= kJitMaxV &&
+          p.E <= kJitMaxE))
+        return false;
+    // only where the parts' slots leave >= 96 lanes per CTA in shared
+    // memory (WS200 at L = 4: ~100 far-read producers x 3 parts -> 64
+    // lanes, slower than the plan walker's global slot tier)
+    const JitOpts o = JitOpts::from_env();
+    const int slots = jit_emit_batched(p, 32, o, nullptr, true);
+    const int64_t head = head_bytes(p, o);
+    const int64_t lanes = (227 * 1024 - 2048 - head) /
+                          std::max<int64_t>(1, per_lane_bytes(p, o, slots, p.pref_ld() + 16, false));
+    return lanes >= 96;
+}
+
+namespace {
+
+struct BatLayout {
+    int64_t ovd = 16, opt = 0, bd = 0, bok = 0, head = 0, ends = 0, avail = 0, tile = 0,
+            tile2 = 0, total = 0;
+    bool bok_on = false;
+};
+
+BatLayout bat_layout(const Plan &p, int T, int slots, int ld_cap, bool dbuf) {
+    BatLayout l;
+    const int NO = p.n_opt, P = p.P;
+    int64_t at = 16;
+    l.ovd = at;
+    at += a16(int64_t(NO) * NO * 2);
+    l.opt = at;
+    at += a16(int64_t(NO) * 8);
+    l.bd = at;
+    at += a16(int64_t(p.V) * NO * P * 8);
+    l.bok_on = !p.latency_complete;
+    if (l.bok_on) {
+        l.bok = at;
+        at += a16(int64_t(p.V) * NO * P);
+    }
+    l.head = at;
+    l.ends = at;
+    at += int64_t(slots) * P * T * 8;
+    l.avail = at;
+    at += int64_t(p.K) * T * 8;
+    at = a16(at);
+    l.tile = at;
+    l.tile2 = dbuf ? at + a16(int64_t(T) * ld_cap) : 0;
+    at += a16(int64_t(T) * ld_cap) * (dbuf ? 2 : 1);
+    l.total = at;
+    return l;
+}
+
+}  // namespace
+
+// Emits the batched kernel for T lanes; returns the number of slots.
+int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, bool dbuf) {
+    const int V = p.V, K = p.K, P = p.P, NO = p.n_opt;
+    std::vector<int> last(V, -1), far_last(V, -1);
+    std::vector<std::vector<int>> preds(V);
+    for (int i = 0; i < V; ++i)
+        for (int e = p.nodes[i].e_begin; e < p.nodes[i].e_end; ++e) {
+            const int q = p.edges[e].gpos;
+            preds[i].push_back(q);
+            last[q] = std::max(last[q], i);
+        }
+    const int near = std::max(1, o.near);
+    for (int i = 0; i < V; ++i)
+        for (int q : preds[i])
+            if (i - q > near) far_last[q] = std::max(far_last[q], i);
+    // interval colouring of the far-read producers' slots
+    std::vector<int> where(V, -1);
+    std::vector<std::vector<int>> dies(V);
+    for (int q = 0; q < V; ++q)
+        if (far_last[q] >= 0) dies[far_last[q]].push_back(q);
+    std::priority_queue<int, std::vector<int>, std::greater<int>> freel;
+    int next = 0;
+    for (int i = 0; i < V; ++i) {
+        for (int q : dies[i]) freel.push(where[q]);
+        if (far_last[i] < 0) continue;
+        if (!freel.empty()) {
+            where[i] = freel.top();
+            freel.pop();
+        } else {
+            where[i] = next++;
+        }
+    }
+    if (src == nullptr) return next;
+    const int ld_cap = p.pref_ld() + 16;
+    const BatLayout l = bat_layout(p, T, next, ld_cap, dbuf);
+    // the option tables
+    std::vector<uint64_t> opt(NO, 0);
+    for (int oo = 0; oo < NO; ++oo)
+        for (int k = 0; k < p.opt_np[oo]; ++k)
+            opt[oo] |= (uint64_t(uint32_t(p.opt_tab[(size_t(oo) * P + k) * 4]) & 0xFFu) |
+                        0x100ull) << (16 * k);
+    std::vector<uint16_t> ovd(size_t(NO) * NO, 0);
+    for (int a = 0; a < NO; ++a)
+        for (int b = 0; b < NO; ++b)
+            for (int m = 0; m < p.opt_np[a]; ++m)
+                for (int k = 0; k < p.opt_np[b]; ++k) {
+                    const int32_t *qa = &p.opt_tab[(size_t(a) * P + m) * 4];
+                    const int32_t *qb = &p.opt_tab[(size_t(b) * P + k) * 4];
+                    const bool overlap = !(qa[2] < qb[1] || qa[1] > qb[2]);
+                    if (overlap && qa[0] != qb[0]) ovd[size_t(a) * NO + b] |= uint16_t(1u << (4 * m + k));
+                }
+    // per-producer om / beta (class 1 of the single bandwidth; 0 when the
+    // mesh has no second device)
+    std::vector<double> cq(V, 0.0);
+    if (p.n_cls > 1)
+        for (int q = 0; q < V; ++q) cq[q] = p.ctab[size_t(q) * p.n_cls + 1];
+    std::string &s = *src;
+    s.clear();
+    char buf[512];
+    s += "#include \"eval_common.cuh\"\nusing namespace hsk;\n";
+    s += "__constant__ unsigned long long HOPT[" + std::to_string(NO) + "] = {";
+    for (int oo = 0; oo < NO; ++oo) s += (oo ? ", " : "") + std::to_string(opt[oo]) + "ull";
+    s += "};\n__constant__ unsigned short HOVD[" + std::to_string(size_t(NO) * NO) + "] = {";
+    for (size_t q = 0; q < ovd.size(); ++q) s += (q ? ", " : "") + std::to_string(ovd[q]);
+    s += "};\n";
+    std::vector<double> cconst;
+    auto cst = [&](double v) {
+        if (!std::isfinite(v)) return lit(v);
+        cconst.push_back(v);
+        return "HSC[" + std::to_string(cconst.size() - 1) + "]";
+    };
+    s += "template <bool TRACE, bool SYNC>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, "
+         "const hs_u8 *g, int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
+         "double &ms_out, int &st_out, double *EG, hs_u32 TB, const double *DG) {\n";
+    s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
+         ") + li;\n    (void)E; (void)EG; (void)TB; (void)DG;\n";
+    s += "    const hs_u16 *OVD = reinterpret_cast<const hs_u16 *>(smem + " +
+         std::to_string(l.ovd) + ");\n";
+    s += "    const unsigned long long *OPT = reinterpret_cast<const unsigned long long *>(smem + " +
+         std::to_string(l.opt) + ");\n";
+    s += "    const double *BD = reinterpret_cast<const double *>(smem + " + std::to_string(l.bd) +
+         ");\n";
+    if (l.bok_on)
+        s += "    const hs_u8 *BOK = smem + " + std::to_string(l.bok) + ";\n";
+    s += "    const hs_u32 A = smem_addr(smem + " + std::to_string(l.avail) + ") + li * 8;\n";
+    for (int k = 0; k < K; ++k)
+        s += "    st_shared_f64(A + " + std::to_string(k * T * 8) + ", 0.0);\n";
+    s += "    int st = 0;\n";
+    const std::string PS = std::to_string(P), NOS = std::to_string(NO);
+    for (int i = 0; i < V; ++i) {
+        const std::string is = std::to_string(i);
+        s += "    // " + p.task_ids[p.order[i]] + "\n";
+        s += "    const int o" + is + " = g[" + is + "];\n";
+        s += "    const unsigned long long W" + is + " = OPT[o" + is + "];\n";
+        for (int k = 0; k < P; ++k)
+            s += "    double r" + is + "_" + std::to_string(k) + " = 0.0;\n";
+        for (size_t e = 0; e < preds[i].size(); ++e) {
+            const int q = preds[i][e];
+            const std::string qs = std::to_string(q);
+            const bool in_reg = i - q <= near;
+            const std::string oq = in_reg ? "o" + qs : "(int)g[" + qs + "]";
+            const std::string mk = "M" + is + "_" + std::to_string(e);
+            s += "    const hs_u32 " + mk + " = OVD[" + oq + " * " + NOS + " + o" + is + "];\n";
+            for (int m = 0; m < P; ++m) {
+                const std::string fv = in_reg
+                    ? "f" + qs + "_" + std::to_string(m)
+                    : "E[" + std::to_string((int64_t(where[q]) * P + m) * T) + "]";
+                for (int k = 0; k < P; ++k) {
+                    std::snprintf(buf, sizeof buf, "(%s & 0x%xu) != 0u", mk.c_str(),
+                                  1u << (4 * m + k));
+                    const std::string r = "r" + is + "_" + std::to_string(k);
+                    s += "    " + r + " = maxsel(" + r + ", " + buf + ", " + fv + ");\n";
+                }
+            }
+        }
+        for (int k = 0; k < P; ++k) {
+            const std::string ks = std::to_string(k), ik = is + "_" + ks;
+            s += "    const int d" + ik + " = (int)((W" + is + " >> " + std::to_string(16 * k) +
+                 ") & 0xFFull);\n";
+            s += "    const bool v" + ik + " = ((W" + is + " >> " + std::to_string(16 * k + 8) +
+                 ") & 1ull) != 0ull;\n";
+            s += "    const hs_u32 A" + ik + " = A + d" + ik + " * " + std::to_string(T * 8) + ";\n";
+            s += "    const double s" + ik + " = pymax(r" + ik + ", ld_shared_f64(A" + ik + "));\n";
+            const std::string bi = "(" + std::to_string(size_t(i) * NO * P + k) + " + o" + is +
+                                   " * " + PS + ")";
+            if (l.bok_on)
+                s += "    st = first_status(st, v" + ik + " && !BOK[" + bi + "], ST_MISSING);\n";
+            s += "    const double e" + ik + " = s" + ik + " + BD[" + bi + "];\n";
+            std::snprintf(buf, sizeof buf,
+                          "    if (TRACE && valid && v%s) starts[(cand * %d + %d) * %d + %d] = s%s;\n",
+                          ik.c_str(), V, i, P, k, ik.c_str());
+            s += buf;
+            s += "    if (v" + ik + ") st_shared_f64(A" + ik + ", e" + ik + ");\n";
+            if (last[i] >= 0) {
+                const bool zero = cq[i] == 0.0 && !std::signbit(cq[i]);
+                s += "    const double f" + ik + " = " +
+                     (zero ? "e" + ik : "e" + ik + " + " + cst(cq[i])) + ";\n";
+                if (where[i] >= 0)
+                    s += "    E[" + std::to_string((int64_t(where[i]) * P + k) * T) + "] = f" + ik +
+                         ";\n";
+            }
+        }
+    }
+    s += "    double ms = 0.0;\n";
+    for (int k = 0; k < K; ++k)
+        s += "    ms = pymax(ms, ld_shared_f64(A + " + std::to_string(k * T * 8) + "));\n";
+    s += "    if (gene_bad) st = ST_GENE;\n"
+         "    ms_out = st ? (st >= ST_MISSING ? knan() : kinf()) : ms;\n"
+         "    st_out = st;\n}\n";
+    if (!cconst.empty()) {
+        std::string decl = "__constant__ double HSC[" + std::to_string(cconst.size()) + "] = {";
+        for (size_t k = 0; k < cconst.size(); ++k) decl += (k ? ", " : "") + lit(cconst[k]);
+        decl += "};\n";
+        const size_t at = s.find("template <bool TRACE");
+        s.insert(at, decl);
+    }
+    s += "template <bool TRACE>\nstruct JitBody {\n  hs_u8 *smem; double *starts; double *eg; "
+         "hs_u32 tb;\n  const double *dg;\n"
+         "  __device__ __forceinline__ void run(const hs_u8 *g, int li, hs_i64 cand, "
+         "bool valid, int gene_bad, double &ms, int &st) {\n"
+         "    jit_body<TRACE, true>(smem, g, li, cand, valid, gene_bad, starts, ms, st, eg, tb, dg);\n"
+         "  }\n};\n";
+    s += "template <bool TRACE>\n__device__ __forceinline__ void jit_main(const EvalParams &a) {\n"
+         "  extern __shared__ __align__(16) hs_u8 smem[];\n";
+    s += "  for (int q = threadIdx.x; q < " + std::to_string(size_t(NO) * NO) +
+         "; q += blockDim.x) reinterpret_cast<hs_u16 *>(smem + " + std::to_string(l.ovd) +
+         ")[q] = HOVD[q];\n";
+    s += "  for (int q = threadIdx.x; q < " + NOS + "; q += blockDim.x) "
+         "reinterpret_cast<unsigned long long *>(smem + " + std::to_string(l.opt) + ")[q] = HOPT[q];\n";
+    s += stage(l.bd, "bdur", int64_t(V) * NO * P * 8);
+    if (l.bok_on) s += stage(l.bok, "bdur_ok", int64_t(V) * NO * P);
+    s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
+         "  body.eg = nullptr;\n  body.tb = 0u;\n  body.dg = nullptr;\n"
+         "  eval_tiles(a, smem, body);\n}\n";
+    std::snprintf(buf, sizeof buf,
+                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
+                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n",
+                  T, T);
+    s += buf;
+    return next;
+}
 
 // Emits the kernel for T lanes; returns the number of shared-memory slots.
 int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
@@ -1000,7 +1264,8 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const JitOpts o = JitOpts::from_env();
-    const int slots = jit_emit(p, 32, o, nullptr);
+    const int slots = p.batched ? jit_emit_batched(p, 32, o, nullptr, true)
+                                : jit_emit(p, 32, o, nullptr);
     const int ld_cap = p.pref_ld() + 16;
     const int64_t head = head_bytes(p, o);
     const int64_t budget = int64_t(optin) - head - 1024;
@@ -1022,7 +1287,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     // too few lanes with the end times in shared memory: move them to the
     // global-memory tier ([slot][lane] per CTA, L2-resident; `gslot_lanes`
     // bounds the footprint SMs x lanes x slots x 8 B)
-    if (T < 128 && slots > 0) {
+    if (T < 128 && slots > 0 && !p.batched) {
         JitOpts og = ob;
         og.gslots = true;
         auto lanes_g = [&](bool db) {
@@ -1041,7 +1306,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     // with its own lane count and long-lived register budget (more warps,
     // fewer registers each); otherwise the shared-memory sizing above stands
     int n_slots = slots;
-    if (o.tmem && !oe.gslots && slots > 0) {
+    if (o.tmem && !oe.gslots && slots > 0 && !p.batched) {
         JitOpts ot = o;
         ot.lanes = o.tm_lanes / o.tm_ctas;
         ot.reg_budget = o.tm_regs;
@@ -1086,7 +1351,10 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     }
     std::string src;
     oe.dbuf = dbuf;
-    jit_emit(p, T, oe, &src);
+    if (p.batched)
+        jit_emit_batched(p, T, oe, &src, dbuf);
+    else
+        jit_emit(p, T, oe, &src);
     const char *hdr_src[] = {kEvalCommonSrc};
     const char *hdr_name[] = {"eval_common.cuh"};
     nvrtcProgram_t prog = nullptr;
@@ -1135,7 +1403,14 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->opts = oe;
     m->ends_global = oe.gslots;
     m->tmem = oe.tmem;
-    {
+    if (p.batched) {
+        const BatLayout l = bat_layout(p, T, n_slots, ld_cap, dbuf);
+        m->smem_tile = l.tile;
+        m->smem_tile2 = l.tile2;
+        m->smem_ends = l.ends;
+        m->smem_kstate = l.avail;
+        m->smem = size_t(l.total);
+    } else {
         const JitLayout l = jit_layout(p, oe, T, n_slots, ld_cap, dbuf);
         m->smem_tile = l.tile;
         m->smem_tile2 = l.tile2;

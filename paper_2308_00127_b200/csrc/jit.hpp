@@ -72,6 +72,8 @@ bool jit_eligible(const Plan &p);
 bool jit_search_ok(const Plan &p);
 // Emits the kernel for T lanes; returns the number of shared-memory slots.
 int jit_emit(const Plan &p, int T, const JitOpts &o, std::string *src);
+// batched-variant plans (extended genomes): the K8 semantics as straight-line code
+int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, bool dbuf);
 int jit_build(const Plan &p, int device, JitModule **out, std::string *err);
 void jit_free(JitModule *m);
 // the launch may use the direct-load kernel (explicit u8 genes, 4-aligned)

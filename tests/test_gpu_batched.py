@@ -120,3 +120,71 @@ def test_global_slot_tier_ws200():
     gg = O.gen_genes(9, 0, n, plan.V, len(opts))
     assert [fhex(x) for x in gm.cpu().numpy()] == \
         [fhex(B.eval_one(inst, 4, opts, r)[0]) for r in gg]
+
+
+def _jit_env(monkeypatch):
+    # specialise every batched plan the test builds, whatever the batch size
+    monkeypatch.setenv("HS_JIT_MIN", "0")
+
+
+def test_specialised_reference_batched_schedules(monkeypatch):
+    """The graph-specialised K8 (jit.cpp, jit_emit_batched) reproduces the
+    reference's bMET / bGreedy schedules: objective and every sub-batch
+    start (trace kernel), on every golden instance it serves."""
+    from paper_2308_00127_b200.batched import _plan
+    _jit_env(monkeypatch)
+    served = 0
+    for e in golden("batched"):
+        g, hw, t = hs.load_instance(e)
+        L = e["L"]
+        plan = _plan(g, hw, t, L, None)
+        if not plan.jit_eligible():
+            continue
+        plan.specialize()
+        served += 1
+        for algo in ("met", "greedy"):
+            res = e[algo]
+            if "error" in res:
+                continue
+            ref = Schedule(batches=tuple(
+                ScheduledBatch(task=b[0], device=b[1], size=b[2],
+                               inputs=tuple(b[3]), start=float.fromhex(b[4]))
+                for b in res["batches"]), objective=0.0, input_count=L)
+            genes = hs.batched_genes_from_schedule(ref, g, hw, t, L)
+            s = hs.decode_batched(genes, g, hw, t, L)
+            assert fhex(s.objective) == res["objective"], (e["name"], algo)
+            got = [[b.task, b.device, b.size, list(b.inputs), fhex(b.start)]
+                   for b in s.batches]
+            assert got == res["batches"], (e["name"], algo)
+    assert served >= 3
+
+
+@pytest.mark.parametrize("name", ["ws30", "rn50f", "iv3f", "ws200"])
+@pytest.mark.parametrize("L", [2, 4, 8])
+def test_specialised_batched_equals_plan_walker(name, L):
+    """Differential: specialised K8 against the plan-walking K8 (pinned to
+    the reference above) on 60,000 random extended genomes, a few of them
+    out of the option range."""
+    from conftest import instance_doc
+    from paper_2308_00127_b200.plan import Plan
+    g, hw, t = hs.load_instance(instance_doc(name))
+    jit = Plan(g, hw, t, L, batched=())
+    aot = Plan(g, hw, t, L, batched=())
+    if not jit.jit_eligible():
+        pytest.skip("too many live part end times for the specialised K8")
+    jit.specialize()
+    no = len(jit.options)
+    rng = np.random.default_rng(L)
+    genes = rng.integers(no, size=(60_000, jit.pref_ld), dtype=np.uint8)
+    genes[::997, 3] = no + 1  # out of range: status 5 on both
+    d = torch.from_numpy(genes).cuda()
+    out = []
+    for plan in (jit, aot):
+        ms = torch.empty(len(genes), dtype=torch.float64, device="cuda")
+        st = torch.empty(len(genes), dtype=torch.uint8, device="cuda")
+        plan.eval(d, ms, st, None)
+        out.append((ms.cpu().numpy(), st.cpu().numpy()))
+    assert np.array_equal(out[0][1], out[1][1])
+    ok = out[0][1] < N.ST_MISSING
+    assert np.array_equal(out[0][0][ok].view(np.uint64),
+                          out[1][0][ok].view(np.uint64))

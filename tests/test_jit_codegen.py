@@ -54,11 +54,21 @@ def test_emit_and_compile(which):
 
 
 def test_scope():
-    # batched-variant plans stay on the AOT kernel
+    # batched-variant plans: specialised on uniform full-mesh platforms
+    # (the CNN / WS instances); per-pair bandwidths stay on the AOT K8
     p = Plan(*hs.load_instance(instance_doc("ws30")), 4, batched=())
-    assert not p.jit_eligible()
+    assert p.jit_eligible()
+    rc, log = _nvrtc_compile(p.specialized_source(128))
+    assert rc == 0, log[-2000:]
+    g, hw, t = hs.load_instance(instance_doc("ws30"))
+    devs = sorted(hw.devices)
+    hw2 = hs.HardwareSystem(list(hw.devices.values()), {
+        (u, v): 1e6 if {u, v} != {devs[0], devs[1]} else 1e5
+        for u in devs for v in devs if u != v})
+    q = Plan(g, hw2, t, 2, batched=())
+    assert not q.jit_eligible()  # two bandwidths
     with pytest.raises(hs.GraphError):
-        p.specialized_source()
+        q.specialized_source()
     assert Plan(*hs.load_instance(instance_doc("ws200")), 1).jit_eligible()
     assert Plan(*hs.load_instance(instance_doc("tf96")), 1).jit_eligible()
     # ~1000 tasks: eligible, with the end-time slots in global memory

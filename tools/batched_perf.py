@@ -29,6 +29,10 @@ for name in sys.argv[1:] or ["rn50f"]:
             print(f"{name} L={L}: {exc}")
             continue
         nopt = len(plan.options)
+        tag = "aot"
+        if os.environ.get("QP_JIT", "1") == "1" and plan.jit_eligible():
+            plan.specialize()
+            tag = "jit"
         genes = torch.randint(0, nopt, (n, plan.pref_ld), dtype=torch.uint8,
                               device="cuda")
         ms = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -51,7 +55,7 @@ for name in sys.argv[1:] or ["rn50f"]:
         e1.record()
         torch.cuda.synchronize()
         dg = e0.elapsed_time(e1) / 1e3
-        print(f"{name} L={L} options={nopt} P={plan.max_parts}: explicit "
+        print(f"{name} [{tag}] L={L} options={nopt} P={plan.max_parts}: explicit "
               f"{n / dt:.3e} cand/s  gen {n / dg:.3e} cand/s", flush=True)
         del genes
         torch.cuda.empty_cache()
