@@ -414,7 +414,7 @@ def graph_rates(stream, gen, world):
             try:
                 g, hw, t = hs.load_instance(_inst(name))
                 plan = _plan(g, hw, t, L, None)
-                out[key] = rate(plan, len(plan.options), 1 << 22, jit=False)
+                out[key] = rate(plan, len(plan.options), 1 << 22)
                 out[key]["options"] = len(plan.options)
                 out[key]["parts"] = plan.max_parts
             except Exception as exc:
