@@ -592,17 +592,23 @@ __device__ __forceinline__ void eval_tiles(const EvalParams &a, hs_u8 *smem, Bod
             // one pass over the lane's own row: flag genes >= K, clamp every
             // byte to K-1 so the specialised code can index by gene freely
             // (rows past the last candidate hold stale bytes)
+            // read-only check; the clamping rewrite only for a row that
+            // holds a gene >= K (the rare error path: status 5)
             hs_u32 *w = reinterpret_cast<hs_u32 *>(row);
             const int nw = (a.V + 3) >> 2;
             const hs_u32 kmax = (hs_u32)(a.gene_range - 1) * 0x01010101u;
             const int tail = a.V & 3;
-            for (int j = 0; j < nw; ++j) {
-                const hs_u32 x = w[j];
-                hs_u32 over = __vcmpgtu4(x, kmax);
-                if (j == nw - 1 && tail) over &= (1u << (8 * tail)) - 1u;
-                gene_bad |= over != 0u;
-                w[j] = __vminu4(x, kmax);
+            hs_u32 any = 0u, over_tail = 0u;
+            for (int j = 0; j + 1 < nw; ++j) any |= __vcmpgtu4(w[j], kmax);
+            if (nw > 0) {
+                over_tail = __vcmpgtu4(w[nw - 1], kmax);
+                if (tail) over_tail &= (1u << (8 * tail)) - 1u;
             }
+            gene_bad = (any | over_tail) != 0u;
+            // bytes past V in the last word are clamped too (the body may
+            // read whole words)
+            if (gene_bad || __vcmpgtu4(nw > 0 ? w[nw - 1] : 0u, kmax))
+                for (int j = 0; j < nw; ++j) w[j] = __vminu4(w[j], kmax);
         }
         double ms;
         int st;
