@@ -1056,10 +1056,12 @@ int jit_emit(const Plan &p, int T, const JitOpts &o_in, std::string *src) {
     // WS1000, whose fetch stalls come from the code streaming through the
     // instruction caches once per tile, and a loss on WS200 -- off by default.
     const int sync_every = std::max(0, o.sync);
+    // a slot written at step q + D is read at step >= q + near + 1: waiting
+    // for the stores every W <= near + 1 - D steps orders every store
+    // before its first load
+    const int wst = std::max(1, std::min(16, near + 1 - D));
     for (int t = 0; t < V + D; ++t) {
-        // a slot written at step q + D is read at step >= q + near + 1:
-        // waiting for the stores every 4 steps orders them when near >= D + 4
-        if (o.tmem && t % 4 == 0 && t > 0) s += "    tm_wait_st();\n";
+        if (o.tmem && t % wst == 0 && t > 0) s += "    tm_wait_st();\n";
         if (t < V) head(t);
         if (t - D >= 0) tail(t - D);
         if (sync_every && t % sync_every == sync_every - 1 && t + 1 < V + D)
