@@ -778,8 +778,9 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
                           budget - stp > 1;
         const int m2 = e.two_level < 16 ? e.two_level : 16;
         const int m = lvl2 ? (m2 < budget - stp - 1 ? m2 : budget - stp - 1) : 0;
-        if (l == 0) {  // speculative moves of the next n steps
-            Pcg64 q = r;
+        Pcg64 q;
+        if (l == 0) {  // speculative moves of the next n steps: step 0 first
+            q = r;
             int pos, nw;
             draw_move(q, pos, nw, -1, 0);
             e.spos[0] = pos;
@@ -791,8 +792,10 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
             }
             (void)q.random();
             if (lvl2) s_q[1][0] = q.slo, s_q[1][1] = q.shi, s_qb[1][0] = q.has, s_qb[1][1] = q.cached;
-            __threadfence_block();
-            if (lvl2) atomicExch(&s_go, 2);  // branch starts published
+        }
+        if (lvl2) __syncthreads();  // the branch starts are published
+        if (l == 0) {  // the remaining base steps
+            int pos, nw;
             for (int i = 1; i < n; ++i) {
                 draw_move(q, pos, nw, -1, 0);
                 e.spos[i] = pos;
@@ -803,10 +806,6 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
             // the two continuation streams, drawn by warps 1 and 2 while
             // thread 0 draws the base steps
             const int b = l == 32 ? 0 : 1;
-            while (atomicAdd(&s_go, 0) != 2) {
-            }
-            __threadfence_block();
-            Pcg64 q;
             q.slo = s_q[b][0];
             q.shi = s_q[b][1];
             q.ilo = e.rng[2];
@@ -823,7 +822,6 @@ __device__ __forceinline__ void sa_chain(const EvalParams &a, const SaParams &e0
             }
         }
         __syncthreads();
-        if (l == 0 && lvl2) s_go = 1;
         const int w0 = l & ~31;
         const bool active = w0 < wb || (lvl2 && w0 == wb);
         if (active) {  // warp-uniform: warps past the window sit out
