@@ -113,6 +113,11 @@ typedef struct hs_best {
 /* thread-local message of the last failure in this thread */
 const char *hs_last_error(void);
 int hs_abi_version(void);
+/* Per-call scratch (speculation buffers, host-pipeline chunks, reductions)
+ * comes from a library-owned stream-ordered pool per device that keeps its
+ * high-water mark between calls; this returns that memory to the driver
+ * (all devices). Call with no library work in flight. */
+int hs_scratch_trim(void);
 
 int hs_plan_create(const hs_instance_desc *desc, hs_plan **out);
 void hs_plan_destroy(hs_plan *plan);
@@ -153,10 +158,17 @@ int hs_eval(const hs_plan *plan, const uint8_t *d_genes, int64_t n, int64_t ld,
 
 /* Same with host buffers; h_genes should be pinned for full PCIe rate.
  * Copies are chunked and overlapped with the kernels on `stream`; returns
- * after the results are in host memory. */
+ * after the results are in host memory. When K <= 4 and the host has >= 8
+ * hardware threads (HS_HOST_PACK=0 / 1 overrides), a pool of host threads
+ * packs the rows to 2 bits per gene into pinned staging while the GPU works
+ * on the previous chunk, so PCIe carries a quarter of the bytes; a chunk
+ * holding a gene >= K is sent unpacked (same statuses as hs_eval). */
 int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
                  int64_t ld, double *h_makespan, uint8_t *h_status,
                  hs_best *h_best, int64_t index_base, void *stream);
+/* 1 when hs_eval_host packs n rows on the host (the rule above), else 0;
+ * negative HS_E* on a bad plan. */
+int hs_eval_host_packs(const hs_plan *plan, int64_t n);
 
 /* 2-bit packed genomes (K <= 4, or <= 4 batched options): gene i of a row
  * is bits 2*(i%4)..2*(i%4)+1 of byte i/4; rows of `ld` bytes with ld % 4

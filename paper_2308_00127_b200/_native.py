@@ -78,6 +78,7 @@ def load() -> C.CDLL:
         sig = {
             "hs_last_error": (C.c_char_p, []),
             "hs_abi_version": (C.c_int, []),
+            "hs_scratch_trim": (C.c_int, []),
             "hs_plan_create": (C.c_int, [_p(InstanceDesc), _p(vp)]),
             "hs_plan_destroy": (None, [vp]),
             "hs_plan_create_batched": (C.c_int, [_p(InstanceDesc), vp, i32,
@@ -90,6 +91,7 @@ def load() -> C.CDLL:
                                                    _p(C.c_int64)]),
             "hs_eval": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
             "hs_eval_host": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
+            "hs_eval_host_packs": (C.c_int, [vp, i64]),
             "hs_eval_packed": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64,
                                          vp]),
             "hs_eval_host_packed": (C.c_int, [vp, vp, i64, i64, vp, vp, vp,
@@ -141,11 +143,12 @@ def load() -> C.CDLL:
 
 def exported_symbols() -> list[str]:
     """Names declared by include/hetsched_b200.h (checked by the tests)."""
-    return ["hs_last_error", "hs_abi_version", "hs_plan_create",
+    return ["hs_last_error", "hs_abi_version", "hs_scratch_trim",
+            "hs_plan_create",
             "hs_plan_destroy", "hs_plan_create_batched",
             "hs_plan_batched_options", "hs_plan_get_info", "hs_plan_order",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
-            "hs_eval_host", "hs_eval_packed", "hs_eval_host_packed",
+            "hs_eval_host", "hs_eval_host_packs", "hs_eval_packed", "hs_eval_host_packed",
             "hs_eval_packed3", "hs_eval_host_packed3", "hs_ea_run",
             "hs_ea_run_chunk", "hs_sa_run", "hs_sa_run_multi",
             "hs_ea_run_multi", "hs_ea_draw", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -14,6 +15,7 @@
 #include "jit.hpp"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "scratch.hpp"
 
 struct hs_plan {
     hs::Plan p;
@@ -52,6 +54,48 @@ uint32_t flags_of(const hs::Plan &p) {
 }  // namespace
 
 namespace hs {
+
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_pool_m;
+cudaMemPool_t g_pools[kMaxDevices] = {};
+}  // namespace
+
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaMallocAsync(p, bytes, s);
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> g(g_pool_m);
+        if (!g_pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            e = cudaMemPoolCreate(&g_pools[dev], &props);
+            if (e != cudaSuccess) {
+                g_pools[dev] = nullptr;
+                return e;
+            }
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = g_pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+int scratch_trim() {
+    std::lock_guard<std::mutex> g(g_pool_m);
+    for (cudaMemPool_t pool : g_pools)
+        if (pool) {
+            const cudaError_t e = cudaMemPoolTrimTo(pool, 0);
+            if (e != cudaSuccess) return cuda_err(e, "hs_scratch_trim");
+        }
+    return HS_OK;
+}
 
 // the thread-local error message of hs_last_error(), for the other
 // translation units of the library (decomp.cpp, validate.cu)
@@ -272,7 +316,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     if (!gen && !packed && n > 0 && (ld > ds->ld_cap || (jm && ld % 4))) {
         // exotic row stride: compact to the preferred stride first
         const int64_t pl = p.pref_ld();
-        CK(cudaMallocAsync(&repack.ptr, size_t(n * pl), stream));
+        CK(hs::scratch_alloc(&repack.ptr, size_t(n * pl), stream));
         CK(cudaMemcpy2DAsync(repack.ptr, size_t(pl), genes, size_t(ld),
                              size_t(p.V), size_t(n), cudaMemcpyDeviceToDevice,
                              stream));
@@ -293,7 +337,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     red.s = stream;
     hs::EvalParams a{};
     if (best) {
-        CK(cudaMallocAsync(&red.ptr, size_t(grid) * sizeof(hs_best) + 16, stream));
+        CK(hs::scratch_alloc(&red.ptr, size_t(grid) * sizeof(hs_best) + 16, stream));
         a.partial = static_cast<hsk::Best *>(red.ptr);
         a.ticket = reinterpret_cast<unsigned int *>(
             static_cast<uint8_t *>(red.ptr) + size_t(grid) * sizeof(hs_best));
@@ -344,7 +388,7 @@ int run_eval(const hs_plan *plan, const uint8_t *genes, int64_t n, int64_t ld,
     ends_g.s = stream;
     if ((jm ? jm->ends_global : ds->ends_global) && n > 0) {
         a.ends_g_cta = int64_t(jm ? jm->slots : p.live_slots) * (p.batched ? p.P : 1) * lanes;
-        CK(cudaMallocAsync(&ends_g.ptr, size_t(grid) * size_t(a.ends_g_cta) * 8, stream));
+        CK(hs::scratch_alloc(&ends_g.ptr, size_t(grid) * size_t(a.ends_g_cta) * 8, stream));
         a.ends_g = static_cast<double *>(ends_g.ptr);
     }
     if (jm) {
@@ -408,7 +452,7 @@ int single_cta_params(const hs_plan *plan, const hs::DevState **dsp, hs::EvalPar
     ends_g.s = stream;
     if (jm ? jm->ends_global : ds->ends_global) {
         a.ends_g_cta = int64_t(a.slots) * a.lanes;
-        CK(cudaMallocAsync(&ends_g.ptr, size_t(a.ends_g_cta) * 8 * size_t(chains), stream));
+        CK(hs::scratch_alloc(&ends_g.ptr, size_t(a.ends_g_cta) * 8 * size_t(chains), stream));
         a.ends_g = static_cast<double *>(ends_g.ptr);
     }
     return HS_OK;
@@ -476,7 +520,7 @@ int run_sa(const hs_plan *plan, uint8_t *genes, uint8_t *best, uint64_t *rng,
     // steps (two-level): [fit f64 | pos i32 | new u8 | status u8]
     e.spec_stride = int64_t(e.window) + 32;
     const size_t nw = size_t(e.spec_stride) * size_t(chains);
-    CK(cudaMallocAsync(&spec.ptr, nw * 16 + 64, stream));
+    CK(hs::scratch_alloc(&spec.ptr, nw * 16 + 64, stream));
     uint8_t *sp = static_cast<uint8_t *>(spec.ptr);
     e.sfit = reinterpret_cast<double *>(sp);
     e.spos = reinterpret_cast<int32_t *>(sp + nw * 8);
@@ -510,6 +554,8 @@ extern "C" {
 const char *hs_last_error(void) { return g_err.c_str(); }
 
 int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+int hs_scratch_trim(void) { return hs::scratch_trim(); }
 
 int hs_plan_create(const hs_instance_desc *desc, hs_plan **out) {
     if (!desc || !out) return set_err(HS_EINVAL, "null argument");
@@ -761,15 +807,15 @@ int eval_host_small(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
     return HS_OK;
 }
 
-// uint8 host genomes (the reference's layout), K <= 4, HS_HOST_PACK=1: the
-// host thread pool packs each chunk to 2 bits per gene into a pinned
+// uint8 host genomes (the reference's layout), K <= 4 (host_pack_enabled):
+// the host thread pool packs each chunk to 2 bits per gene into a pinned
 // staging buffer while the GPU copies and evaluates the previous one
 // (double-buffered), so the PCIe link carries ceil(V/4) instead of V bytes
-// per candidate. It pays only where the host threads read memory faster
-// than the copy engine does (not on this pool's 16-vCPU hosts: 1.3e8 vs
-// 2.7e8 candidates/s, profiles r2f), hence opt-in. A chunk holding a gene
-// >= K goes over unpacked, so the kernel flags it (status 5) exactly as on
-// the unpacked path.
+// per candidate. The call is then bound by the host threads' read rate of
+// the uint8 rows (r3u: 3.0-3.2e8 candidates/s on 16 vCPUs against 2.67e8
+// for the DMA of the bytes). A chunk holding a gene >= K goes over
+// unpacked, so the kernel flags it (status 5) exactly as on the unpacked
+// path.
 int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, int64_t ld,
                         double *h_makespan, uint8_t *h_status, hs_best *h_best,
                         int64_t index_base, cudaStream_t s0) {
@@ -794,9 +840,9 @@ int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, 
         cudaError_t e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
         for (auto &c : copied)
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaMallocAsync((void **)&buf, 2 * per, s0);
+        if (e == cudaSuccess) e = hs::scratch_alloc((void **)&buf, 2 * per, s0);
         if (e == cudaSuccess)
-            e = cudaMallocAsync((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
+            e = hs::scratch_alloc((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
         if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ss[1], ev0, 0);
         if (e != cudaSuccess) {
@@ -871,10 +917,12 @@ bool host_pack_enabled(const hs::Plan &p, int64_t n, int packed) {
     if (packed || p.batched || p.K > 4 || p.V < 16 || n <= kSmallN) return false;
     const int64_t pld = ((p.V + 3) / 4 + 3) / 4 * 4;
     if (pld > p.pref_ld() || pld > 256) return false;
-    // opt-in: on the pool's hosts the CPU threads read the uint8 rows at
-    // ~27 GB/s while the copy engine reads them at ~54 GB/s (profiles r2f)
+    // on by default with >= 8 host threads: r3t measured 3.35e8 cand/s
+    // packed on 16 threads against 2.67e8 for the uint8 DMA (WS200, 8.4 M
+    // rows per call), once the device scratch stays mapped between calls
     const char *v = getenv("HS_HOST_PACK");
-    return v && std::atoi(v) != 0;
+    if (v && *v) return std::atoi(v) != 0;
+    return hs::host_pack_threads() >= 8;
 }
 
 }  // namespace
@@ -909,9 +957,9 @@ static int eval_host_impl(const hs_plan *plan, const uint8_t *h_genes, int64_t n
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev0, 0);
-        if (e == cudaSuccess) e = cudaMallocAsync((void **)&buf, 2 * per, s0);
+        if (e == cudaSuccess) e = hs::scratch_alloc((void **)&buf, 2 * per, s0);
         if (e == cudaSuccess)
-            e = cudaMallocAsync((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
+            e = hs::scratch_alloc((void **)&bests, size_t(nchunks) * sizeof(hs_best), s0);
         if (e == cudaSuccess) e = cudaEventRecord(ev0, s0);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev0, 0);
         if (e != cudaSuccess) {
@@ -978,6 +1026,12 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
                  hs_best *h_best, int64_t index_base, void *stream) {
     return eval_host_impl(plan, h_genes, n, ld, h_makespan, h_status, h_best,
                           index_base, stream, 0);
+}
+
+int hs_eval_host_packs(const hs_plan *plan, int64_t n) {
+    if (!plan) return set_err(HS_EINVAL, "null plan");
+    if (n <= kSmallN || plan->p.V <= 0) return 0;
+    return host_pack_enabled(plan->p, n, 0) ? 1 : 0;
 }
 
 int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
@@ -1058,7 +1112,7 @@ int hs_cp_bound(const hs_plan *plan, const uint64_t *d_masks, int64_t nsub,
         1, std::min<int64_t>(nsub, (int64_t(1) << 25) / std::max(p.V, 1)));
     Scratch sc;
     sc.s = s;
-    CK(cudaMallocAsync(&sc.ptr, size_t(std::max(p.V, 1)) * size_t(step) * 8, s));
+    CK(hs::scratch_alloc(&sc.ptr, size_t(std::max(p.V, 1)) * size_t(step) * 8, s));
     for (int64_t lo = 0; lo < nsub; lo += step) {
         const int64_t m = std::min(step, nsub - lo);
         rc = hs::launch_cp(ds->blob, p.lay, p.V, std::max(p.words, 1),
@@ -1198,7 +1252,7 @@ extern "C" int hs_best_allreduce(const hs_best *d_in, hs_best *d_out, ncclComm *
                                      (api.errstr ? api.errstr(nr) : "failed"));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     hs_best *all = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void **>(&all), sizeof(hs_best) * size_t(nranks), s));
+    CK(hs::scratch_alloc(reinterpret_cast<void **>(&all), sizeof(hs_best) * size_t(nranks), s));
     nr = api.allgather(d_in, all, 2, kNcclInt64, comm, s);
     if (nr != 0) {
         cudaFreeAsync(all, s);

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/hetsched_b200.h"
+#include "scratch.hpp"
 
 namespace hs {
 int set_error(int code, const std::string &msg);
@@ -433,7 +434,7 @@ extern "C" int hs_validate_schedules(const hs_instance_desc *d, int64_t n_sched,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DevBuf buf;
     buf.s = s;
-    cudaError_t e = cudaMallocAsync(&buf.p, total, s);
+    cudaError_t e = hs::scratch_alloc(&buf.p, total, s);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(buf.p, host.data(), upload_end, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess)

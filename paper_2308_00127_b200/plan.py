@@ -252,6 +252,13 @@ class Plan:
             C.byref(best) if best is not None else None, int(index_base),
             self._stream(stream)), "hs_eval_host")
 
+    def eval_host_packs(self, n: int) -> bool:
+        """hs_eval_host_packs: whether eval_host packs n rows on the host."""
+        rc = int(self._lib.hs_eval_host_packs(self.handle, int(n)))
+        if rc < 0:
+            N.check(rc, "hs_eval_host_packs")
+        return rc == 1
+
     def packed_ld(self) -> int:
         """Row bytes of 2-bit packed genomes (multiple of 4)."""
         return ((self.V + 3) // 4 + 3) // 4 * 4

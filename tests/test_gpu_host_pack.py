@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _host(plan, genes, monkeypatch, pack):
-    monkeypatch.setenv("HS_HOST_PACK", "1" if pack else "0")  # opt-in path
+    monkeypatch.setenv("HS_HOST_PACK", "1" if pack else "0")  # forced either way
     n = len(genes)
     ms = np.empty(n, np.float64)
     st = np.empty(n, np.uint8)

@@ -118,3 +118,21 @@ def test_pack_genes_layouts():
         assert np.array_equal(d2.reshape(17, -1)[:, :V], genes)
     with pytest.raises(hs.GraphError):
         hs.pack_genes3(np.full((1, 4), 3, np.uint8))
+
+
+def test_host_pack_policy(monkeypatch):
+    """hs_eval_host packs on the host by default when K <= 4 and the host
+    has >= 8 threads; HS_HOST_PACK=0 / 1 override; small batches and K > 4
+    never pack (hs_eval_host_packs reports the decision, host-only)."""
+    g, hw, t = hs.load_instance(instance_doc("ws200"))
+    plan = Plan(g, hw, t, 1)
+    n = 1 << 20
+    monkeypatch.delenv("HS_HOST_PACK", raising=False)
+    assert plan.eval_host_packs(n) == ((os.cpu_count() or 1) >= 8)
+    assert not plan.eval_host_packs(1000)
+    monkeypatch.setenv("HS_HOST_PACK", "0")
+    assert not plan.eval_host_packs(n)
+    monkeypatch.setenv("HS_HOST_PACK", "1")
+    assert plan.eval_host_packs(n)
+    g, hw, t = hs.load_instance(instance_doc("tf96"))
+    assert not Plan(g, hw, t, 1).eval_host_packs(n)  # K = 30

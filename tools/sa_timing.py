@@ -2,6 +2,9 @@
 of SA / EA on one instance: separates GPU-side from host-side variance.
 
     python tools/sa_timing.py [instance] [reps]
+
+SLEEP_CYCLES=N queues a busy-wait of N cycles before the start event, so the
+host's launch preparation overlaps it and the events time the kernel alone.
 """
 import os
 import sys
@@ -25,8 +28,13 @@ orig = H.Plan.sa_run
 dev_ms = []
 
 
+SLEEP = int(os.environ.get("SLEEP_CYCLES", "0"))
+
+
 def timed(self, *a, **k):
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if SLEEP:  # keep the GPU busy while the host prepares the launch, so
+        torch.cuda._sleep(SLEEP)  # the events bracket device time only
     s0.record()
     orig(self, *a, **k)
     s1.record()
