@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -849,7 +851,11 @@ int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, 
             rc = cuda_err(e, "hs_eval_host (packing) setup");
             break;
         }
+        double t_wait = 0, t_pack = 0, t_enq = 0;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
         for (int64_t c = 0; c < nchunks && rc == HS_OK; ++c) {
+            auto q0 = now();
             const int k = int(c & 1);
             cudaStream_t s = ss[k];
             uint8_t *b = buf + k * per;
@@ -864,7 +870,10 @@ int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, 
                     break;
                 }
             }
+            auto q1 = now();
             const bool ok = hs::pack2_rows(h_genes + lo * ld, ld, V, p.K, rows, stage[k], pld);
+            auto q2 = now();
+            t_wait += sec(q0, q1); t_pack += sec(q1, q2);
             if (ok)
                 e = cudaMemcpyAsync(b, stage[k], size_t(rows * pld), cudaMemcpyHostToDevice, s);
             else
@@ -887,7 +896,9 @@ int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, 
                 e = cudaMemcpyAsync(h_status + lo, dsx, size_t(rows), cudaMemcpyDeviceToHost,
                                     s);
             if (e != cudaSuccess) rc = cuda_err(e, "D2H results");
+            t_enq += sec(q2, now());
         }
+        auto q3 = now();
         if (rc) break;
         e = cudaEventRecord(ev0, ss[1]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, ev0, 0);
@@ -901,6 +912,9 @@ int eval_host_u8_packed(const hs_plan *plan, const uint8_t *h_genes, int64_t n, 
             break;
         }
         if (h_best) hs_best_merge(hb.data(), nchunks, h_best);
+        if (getenv("HS_PACK_TRACE"))
+            fprintf(stderr, "pack trace: wait %.2f pack %.2f enqueue %.2f drain %.2f ms\n",
+                    t_wait * 1e3, t_pack * 1e3, t_enq * 1e3, sec(q3, now()) * 1e3);
     } while (0);
     if (buf) cudaFreeAsync(buf, s0);
     if (bests) cudaFreeAsync(bests, s0);

@@ -25,7 +25,13 @@
 namespace hs {
 namespace {
 
-// A fixed pool of worker threads running index ranges of one job at a time.
+// A fixed pool of worker threads running the parts of one job at a time.
+// Parts are claimed from a counter tagged with the job number, so a worker
+// that wakes late for a finished job can never run a part of the next one;
+// workers spin ~100 us on the job number before sleeping (the host-packing
+// pipeline issues its chunks back to back, and a condition-variable wake-up
+// of 15 threads per chunk cost ~0.25 ms, r3y), and the caller spins on the
+// pending count.
 class Pool {
   public:
     explicit Pool(int n) {
@@ -34,7 +40,7 @@ class Pool {
     ~Pool() {
         {
             std::lock_guard<std::mutex> g(m_);
-            stop_ = true;
+            stop_.store(true);
         }
         cv_.notify_all();
         for (auto &t : workers_) t.join();
@@ -42,52 +48,62 @@ class Pool {
     int size() const { return int(workers_.size()) + 1; }
     // fn(part) for part in [0, parts), the caller thread taking part too
     void run(int parts, const std::function<void(int)> &fn) {
-        std::unique_lock<std::mutex> lk(job_m_);  // one job at a time
+        std::lock_guard<std::mutex> lk(job_m_);  // one job at a time
+        const uint64_t j = job_.load(std::memory_order_relaxed) + 1;
+        fn_.store(&fn, std::memory_order_relaxed);
+        parts_.store(parts, std::memory_order_relaxed);
+        pending_.store(parts, std::memory_order_relaxed);
+        next_.store(j << 32, std::memory_order_release);
         {
             std::lock_guard<std::mutex> g(m_);
-            fn_ = &fn;
-            parts_ = parts;
-            next_.store(0);
-            pending_ = parts;
-            ++gen_;
+            job_.store(j, std::memory_order_release);
         }
         cv_.notify_all();
-        work();
-        std::unique_lock<std::mutex> g(m_);
-        done_cv_.wait(g, [this] { return pending_ == 0; });
-        fn_ = nullptr;
+        work(j);
+        while (pending_.load(std::memory_order_acquire) > 0) _mm_pause();
     }
 
   private:
-    void work() {
+    static constexpr int kSpin = 2000;
+    void work(uint64_t j) {
         for (;;) {
-            const int k = next_.fetch_add(1);
-            if (k >= parts_) return;
-            (*fn_)(k);
-            std::lock_guard<std::mutex> g(m_);
-            if (--pending_ == 0) done_cv_.notify_all();
+            uint64_t v = next_.load(std::memory_order_acquire);
+            for (;;) {
+                if ((v >> 32) != j ||
+                    uint32_t(v) >= uint32_t(parts_.load(std::memory_order_relaxed)))
+                    return;
+                if (next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel)) break;
+            }
+            (*fn_.load(std::memory_order_relaxed))(int(uint32_t(v)));
+            pending_.fetch_sub(1, std::memory_order_release);
         }
     }
     void loop() {
         uint64_t seen = 0;
         for (;;) {
-            {
-                std::unique_lock<std::mutex> g(m_);
-                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
-                if (stop_) return;
-                seen = gen_;
+            uint64_t j = job_.load(std::memory_order_acquire);
+            for (int i = 0; j == seen && i < kSpin && !stop_.load(); ++i) {
+                _mm_pause();
+                j = job_.load(std::memory_order_acquire);
             }
-            work();
+            if (j == seen) {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_.load() || job_.load() != seen; });
+                if (stop_.load()) return;
+                j = job_.load(std::memory_order_acquire);
+            }
+            if (stop_.load()) return;
+            seen = j;
+            work(j);
         }
     }
     std::vector<std::thread> workers_;
     std::mutex m_, job_m_;
-    std::condition_variable cv_, done_cv_;
-    const std::function<void(int)> *fn_ = nullptr;
-    std::atomic<int> next_{0};
-    int parts_ = 0, pending_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::condition_variable cv_;
+    std::atomic<const std::function<void(int)> *> fn_{nullptr};
+    std::atomic<uint64_t> next_{0}, job_{0};
+    std::atomic<int> parts_{0}, pending_{0};
+    std::atomic<bool> stop_{false};
 };
 
 Pool &pool() {
@@ -164,7 +180,8 @@ __attribute__((target("avx2"))) uint64_t pack_rows_avx2(const uint8_t *src, int6
     const int tail_bytes = int(pld) - o_t;  // packed tail + zero padding
     const __m256i tmask =
         _mm256_loadu_si256(reinterpret_cast<const __m256i *>(ones + 32 - t));
-    const int64_t pf_dist = std::max<int64_t>(2, 4096 / ld) * ld;
+    static const int64_t pf_bytes = getenv("HS_PACK_PF") ? atoll(getenv("HS_PACK_PF")) : 4096;
+    const int64_t pf_dist = std::max<int64_t>(2, pf_bytes / ld) * ld;
     __m256i mx = _mm256_setzero_si256();
     uint64_t bad = 0;
     for (int64_t r = r0; r < r1; ++r) {
