@@ -170,6 +170,16 @@ int hs_eval_host(const hs_plan *plan, const uint8_t *h_genes, int64_t n,
  * negative HS_E* on a bad plan. */
 int hs_eval_host_packs(const hs_plan *plan, int64_t n);
 
+/* Host-only: the packer hs_eval_host runs on its thread pool, for callers
+ * that keep genomes packed (hs_eval_packed / hs_eval_host_packed input).
+ * n rows of V uint8 genes (row stride ld) -> n rows of pld bytes, gene i in
+ * bits 2*(i%4) of byte i/4, bytes past ceil(V/4) zero. *all_ok = 0 when
+ * some gene is >= K (those bytes are then unspecified). No CUDA calls.
+ * Replaces nothing in the reference (its genomes are Python lists,
+ * heuristics.py:24-40); see heuristics.pack_genes. */
+int hs_pack_genes2(const uint8_t *h_genes, int64_t n, int64_t ld, int32_t V,
+                   int32_t K, uint8_t *h_packed, int64_t pld, int32_t *all_ok);
+
 /* 2-bit packed genomes (K <= 4, or <= 4 batched options): gene i of a row
  * is bits 2*(i%4)..2*(i%4)+1 of byte i/4; rows of `ld` bytes with ld % 4
  * == 0 and ceil(V/4) <= ld <= pref_ld. A quarter of the bytes of hs_eval's

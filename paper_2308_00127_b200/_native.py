@@ -92,6 +92,8 @@ def load() -> C.CDLL:
             "hs_eval": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
             "hs_eval_host": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
             "hs_eval_host_packs": (C.c_int, [vp, i64]),
+            "hs_pack_genes2": (C.c_int, [vp, i64, i64, i32, i32, vp, i64,
+                                         _p(C.c_int32)]),
             "hs_eval_packed": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, i64,
                                          vp]),
             "hs_eval_host_packed": (C.c_int, [vp, vp, i64, i64, vp, vp, vp,
@@ -148,7 +150,7 @@ def exported_symbols() -> list[str]:
             "hs_plan_destroy", "hs_plan_create_batched",
             "hs_plan_batched_options", "hs_plan_get_info", "hs_plan_order",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
-            "hs_eval_host", "hs_eval_host_packs", "hs_eval_packed", "hs_eval_host_packed",
+            "hs_eval_host", "hs_eval_host_packs", "hs_pack_genes2", "hs_eval_packed", "hs_eval_host_packed",
             "hs_eval_packed3", "hs_eval_host_packed3", "hs_ea_run",
             "hs_ea_run_chunk", "hs_sa_run", "hs_sa_run_multi",
             "hs_ea_run_multi", "hs_ea_draw", "hs_eval_gen", "hs_eval_gen_ex", "hs_trace",

@@ -1048,6 +1048,17 @@ int hs_eval_host_packs(const hs_plan *plan, int64_t n) {
     return host_pack_enabled(plan->p, n, 0) ? 1 : 0;
 }
 
+int hs_pack_genes2(const uint8_t *h_genes, int64_t n, int64_t ld, int32_t V, int32_t K,
+                   uint8_t *h_packed, int64_t pld, int32_t *all_ok) {
+    if (n < 0 || V <= 0 || K < 1 || K > 4 || ld < V || pld < (V + 3) / 4)
+        return set_err(HS_EINVAL, "hs_pack_genes2: need n >= 0, V > 0, 1 <= K <= 4, "
+                                  "ld >= V, pld >= ceil(V/4)");
+    if (n > 0 && (!h_genes || !h_packed)) return set_err(HS_EINVAL, "hs_pack_genes2: null buffer");
+    const bool ok = n == 0 || hs::pack2_rows(h_genes, ld, V, K, n, h_packed, pld);
+    if (all_ok) *all_ok = ok ? 1 : 0;
+    return HS_OK;
+}
+
 int hs_eval_host_packed(const hs_plan *plan, const uint8_t *h_packed, int64_t n,
                         int64_t ld, double *h_makespan, uint8_t *h_status,
                         hs_best *h_best, int64_t index_base, void *stream) {

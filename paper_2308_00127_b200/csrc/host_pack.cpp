@@ -26,8 +26,11 @@ namespace hs {
 namespace {
 
 // A fixed pool of worker threads running the parts of one job at a time.
-// Parts are claimed from a counter tagged with the job number, so a worker
-// that wakes late for a finished job can never run a part of the next one;
+// Parts are claimed from one 64-bit word holding the job number, the job's
+// part count and the claim counter, so a worker that wakes late for a
+// finished job can never run a part of the next one (the count is read
+// from the same word it claims with, never from a separately published
+// field the next job may already have overwritten);
 // workers spin ~100 us on the job number before sleeping (the host-packing
 // pipeline issues its chunks back to back, and a condition-variable wake-up
 // of 15 threads per chunk cost ~0.25 ms, r3y), and the caller spins on the
@@ -51,9 +54,8 @@ class Pool {
         std::lock_guard<std::mutex> lk(job_m_);  // one job at a time
         const uint64_t j = job_.load(std::memory_order_relaxed) + 1;
         fn_.store(&fn, std::memory_order_relaxed);
-        parts_.store(parts, std::memory_order_relaxed);
         pending_.store(parts, std::memory_order_relaxed);
-        next_.store(j << 32, std::memory_order_release);
+        next_.store((j << 32) | (uint64_t(parts) << 16), std::memory_order_release);
         {
             std::lock_guard<std::mutex> g(m_);
             job_.store(j, std::memory_order_release);
@@ -67,14 +69,14 @@ class Pool {
     static constexpr int kSpin = 2000;
     void work(uint64_t j) {
         for (;;) {
+            // next_ = job << 32 | parts << 16 | claimed
             uint64_t v = next_.load(std::memory_order_acquire);
             for (;;) {
-                if ((v >> 32) != j ||
-                    uint32_t(v) >= uint32_t(parts_.load(std::memory_order_relaxed)))
-                    return;
+                if ((v >> 32) != j || (v & 0xFFFFu) >= ((v >> 16) & 0xFFFFu)) return;
                 if (next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel)) break;
             }
-            (*fn_.load(std::memory_order_relaxed))(int(uint32_t(v)));
+            // a claimed part keeps job j unfinished, so fn_ is still job j's
+            (*fn_.load(std::memory_order_relaxed))(int(v & 0xFFFFu));
             pending_.fetch_sub(1, std::memory_order_release);
         }
     }
@@ -102,7 +104,7 @@ class Pool {
     std::condition_variable cv_;
     std::atomic<const std::function<void(int)> *> fn_{nullptr};
     std::atomic<uint64_t> next_{0}, job_{0};
-    std::atomic<int> parts_{0}, pending_{0};
+    std::atomic<int> pending_{0};
     std::atomic<bool> stop_{false};
 };
 
@@ -155,8 +157,9 @@ inline uint64_t pack_row(const uint8_t *src, int V, uint8_t *dst, int pld, uint6
 // (b0 + 4 b1) + 16 (b2 + 4 b3), then 32 -> 16 -> 8-bit packs). The row's
 // last < 32 genes come from one 32-byte load masked to the row (the bytes
 // past it belong to the next row, so only the very last row of the buffer
-// takes the scalar tail); genes >= K are found by one unsigned max kept
-// across all rows of the range.
+// takes the scalar tail: any row whose 32-byte tail load would run past
+// `end`, the readable bytes of the buffer); genes >= K are found by one
+// unsigned max kept across all rows of the range.
 __attribute__((target("avx2"))) inline __m256i pack32_avx2(__m256i x) {
     const __m256i m14 = _mm256_set1_epi16(0x0401);       // bytes (1, 4)
     const __m256i m116 = _mm256_set1_epi32(0x00100001);  // words (1, 16)
@@ -170,7 +173,7 @@ __attribute__((target("avx2"))) inline __m256i pack32_avx2(__m256i x) {
 
 __attribute__((target("avx2"))) uint64_t pack_rows_avx2(const uint8_t *src, int64_t ld,
                                                          int V, int K, int64_t r0, int64_t r1,
-                                                         bool last_is_end, uint8_t *dst,
+                                                         int64_t end, uint8_t *dst,
                                                          int64_t pld, uint64_t kadd) {
     alignas(32) static const uint8_t ones[64] = {
         0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0xFF,
@@ -200,7 +203,7 @@ __attribute__((target("avx2"))) uint64_t pack_rows_avx2(const uint8_t *src, int6
         }
         if (t == 0) {
             for (; o < pld; ++o) d[o] = 0;
-        } else if (r + 1 < r1 || !last_is_end) {
+        } else if (r * ld + i + 32 <= end) {
             const __m256i x = _mm256_and_si256(
                 _mm256_loadu_si256(reinterpret_cast<const __m256i *>(s + i)), tmask);
             mx = _mm256_max_epu8(mx, x);
@@ -227,14 +230,15 @@ bool pack2_rows(const uint8_t *src, int64_t ld, int V, int K, int64_t rows, uint
     const uint64_t kadd = uint64_t(0x80 - K) * 0x0101010101010101ull;
     static const bool avx2 = __builtin_cpu_supports("avx2");
     Pool &pl = pool();
-    const int parts = int(std::min<int64_t>(rows, int64_t(pl.size()) * 4));
+    // (at most 65535 parts: the claim word's 16-bit fields)
+    const int parts = int(std::min<int64_t>({rows, int64_t(pl.size()) * 4, 65535}));
     if (parts <= 0) return true;
     std::atomic<uint64_t> bad{0};
     pl.run(parts, [&](int k) {
         const int64_t a = rows * k / parts, b = rows * (k + 1) / parts;
         uint64_t bd = 0;
         if (avx2)
-            bd = pack_rows_avx2(src, ld, V, K, a, b, b == rows, dst, pld, kadd);
+            bd = pack_rows_avx2(src, ld, V, K, a, b, (rows - 1) * ld + V, dst, pld, kadd);
         else
             for (int64_t r = a; r < b; ++r)
                 bd |= pack_row(src + r * ld, V, dst + r * pld, int(pld), kadd);

@@ -239,17 +239,30 @@ def fitness_batch(genes, g, hw, table, L: int, *,
 
 def pack_genes(genes: np.ndarray) -> np.ndarray:
     """2-bit packing of uint8 genes < 4 [n, V] -> [n, ceil(ceil(V/4)/4)*4]:
-    gene i in bits 2*(i%4) of byte i//4 (hs_eval_packed's layout)."""
+    gene i in bits 2*(i%4) of byte i//4 (hs_eval_packed's layout), by the
+    native host packer hs_eval_host uses (hs_pack_genes2: AVX2, thread
+    pool)."""
+    import ctypes as C
+    if isinstance(genes, np.ndarray) and genes.dtype != np.uint8:
+        if genes.size and (genes.min() < 0 or genes.max() > 3):
+            raise GraphError("2-bit packing needs genes < 4")
     genes = np.asarray(genes, np.uint8)
+    if genes.ndim != 2:
+        raise GraphError("pack_genes: genes must be [n, V]")
+    if genes.strides[1] != 1 or genes.strides[0] < genes.shape[1]:
+        genes = np.ascontiguousarray(genes)
     n, V = genes.shape
-    if genes.size and genes.max() > 3:
-        raise GraphError("2-bit packing needs genes < 4")
     pld = ((V + 3) // 4 + 3) // 4 * 4
-    g = np.zeros((n, pld * 4), np.uint8)
-    g[:, :V] = genes
-    g = g.reshape(n, pld, 4)
-    return (g[:, :, 0] | (g[:, :, 1] << 2) | (g[:, :, 2] << 4)
-            | (g[:, :, 3] << 6)).astype(np.uint8)
+    out = np.zeros((n, pld), np.uint8)
+    if n == 0 or V == 0:
+        return out
+    ok = C.c_int32(0)
+    N.check(N.load().hs_pack_genes2(genes.ctypes.data, n, genes.strides[0], V,
+                                    4, out.ctypes.data, pld, C.byref(ok)),
+            "pack_genes")
+    if not ok.value:
+        raise GraphError("2-bit packing needs genes < 4")
+    return out
 
 
 def pack_genes3(genes: np.ndarray) -> np.ndarray:

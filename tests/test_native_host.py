@@ -136,3 +136,76 @@ def test_host_pack_policy(monkeypatch):
     assert plan.eval_host_packs(n)
     g, hw, t = hs.load_instance(instance_doc("tf96"))
     assert not Plan(g, hw, t, 1).eval_host_packs(n)  # K = 30
+
+
+def _pack2_ref(genes, pld):
+    n, V = genes.shape
+    g = np.zeros((n, pld * 4), np.uint8)
+    g[:, :V] = genes
+    g = g.reshape(n, pld, 4)
+    return (g[:, :, 0] | (g[:, :, 1] << 2) | (g[:, :, 2] << 4)
+            | (g[:, :, 3] << 6)).astype(np.uint8)
+
+
+def test_host_packer_matches_numpy():
+    """hs_pack_genes2 (the AVX2 thread-pool packer inside hs_eval_host)
+    equals a numpy restatement of the 2-bit layout on ragged widths, row
+    strides past V and row counts that split unevenly over the pool; an
+    out-of-range gene anywhere (incl. the last row's tail) is reported."""
+    import ctypes as C
+    lib = _native.load()
+    rng = np.random.default_rng(5)
+    for V in (1, 3, 5, 17, 31, 32, 33, 63, 64, 202, 1002):
+        for n in (1, 2, 7, 64, 1000, 4099):
+            for extra in (0, 3, 29):
+                ld = V + extra
+                K = int(rng.integers(1, 5))
+                buf = rng.integers(0, K, size=n * ld, dtype=np.uint8)
+                # the buffer ends at the last gene byte (no slack after it)
+                buf = buf[:(n - 1) * ld + V].copy()
+                pld = ((V + 3) // 4 + 3) // 4 * 4
+                out = np.full((n, pld), 0xAA, np.uint8)
+                ok = C.c_int32(-1)
+                assert lib.hs_pack_genes2(buf.ctypes.data, n, ld, V, K,
+                                          out.ctypes.data, pld, C.byref(ok)) == 0
+                rows = np.lib.stride_tricks.as_strided(buf, (n, V), (ld, 1))
+                assert ok.value == 1
+                assert np.array_equal(out, _pack2_ref(rows, pld)), (V, n, extra)
+                if K < 4:
+                    for r, c in ((n - 1, V - 1), (0, 0), (n // 2, V // 2)):
+                        bad = buf.copy()
+                        bad[r * ld + c] = K
+                        assert lib.hs_pack_genes2(bad.ctypes.data, n, ld, V, K,
+                                                  out.ctypes.data, pld,
+                                                  C.byref(ok)) == 0
+                        assert ok.value == 0, (V, n, extra, r, c)
+    assert lib.hs_pack_genes2(None, 1, 4, 4, 5, None, 4, None) != 0
+
+
+def test_host_packer_back_to_back_jobs():
+    """Many small packing jobs issued back to back (the pool's workers wake
+    late for finished jobs while the next one is published) and from two
+    Python threads at once: every result equals the numpy packing."""
+    import threading
+    rng = np.random.default_rng(9)
+    cases = [rng.integers(0, 4, size=(int(rng.integers(1, 300)),
+                                      int(rng.integers(1, 90))), dtype=np.uint8)
+             for _ in range(60)]
+    want = [_pack2_ref(g, ((g.shape[1] + 3) // 4 + 3) // 4 * 4) for g in cases]
+    errors = []
+
+    def worker(rounds):
+        for _ in range(rounds):
+            for g, w in zip(cases, want):
+                if not np.array_equal(hs.pack_genes(g), w):
+                    errors.append(g.shape)
+    ts = [threading.Thread(target=worker, args=(15,)) for _ in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:5]
+    with pytest.raises(hs.GraphError):
+        hs.pack_genes(np.full((2, 9), 4, np.uint8))
+    with pytest.raises(hs.GraphError):
+        hs.pack_genes(np.full((2, 9), 256, np.int64))
