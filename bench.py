@@ -425,7 +425,7 @@ def graph_rates(stream, gen, world):
 
 def n_sweep(stream, world, rank, comm):
     """Config 5: 1e6 .. 1e9 on-device generated WS200 candidates
-    (hs_eval_gen: oracle.gen_genes's splitmix64 counter hash, genomes never
+    (hs_eval_gen: oracle.gen_genes's counter hash, genomes never
     touch HBM), this rank's contiguous shard, best merged over ranks on the
     device; a few sampled candidates' genomes and makespans are kept for the
     CPU re-scoring in cpu_baseline."""

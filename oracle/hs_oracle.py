@@ -29,7 +29,8 @@ What is restated (reference = /root/reference/pkg/src/hetsched):
 * ``critical_path`` -- ``bounds.py:57-72``; ``reach_dep``/``reach_pre`` --
   ``bounds.py:29-54``.
 * ``gen_genes`` -- the on-device candidate generator's counter hash
-  (splitmix64) so any generated candidate can be re-derived.
+  (splitmix64 per candidate + a multiply-xorshift per 8 genes)
+  so any generated candidate can be re-derived.
 
 Status codes (shared with the CUDA path): 0 feasible, 1 unsupported batch
 size, 2 memory, 3 missing link, 4 missing latency entry (GraphError),
@@ -343,6 +344,8 @@ def reach_pre(inst: Instance, u, T):
 # --------------------------------------------------- on-device generator
 M64 = (1 << 64) - 1
 GOLDEN = 0x9E3779B97F4A7C15
+GEN_C1 = 0xD1B54A32D192ED03
+GEN_C2 = 0xD6E8FEB86659FD93
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:
@@ -355,17 +358,19 @@ def splitmix64(x: np.ndarray) -> np.ndarray:
 
 
 def gen_genes(seed: int, first: int, n: int, V: int, K: int) -> np.ndarray:
-    """Candidate c (global index) position i gets
-    ((h >> 16*(i%4)) & 0xFFFF) * K >> 16 with
-    h = splitmix64(seed + (c*W + i//4 + 1) * GOLDEN), W = ceil(V/4)."""
-    W = (V + 3) // 4
+    """Candidate c (global index): h = splitmix64(seed + (c+1)*GOLDEN); for
+    w = 0, 1, ..: z = h + (w+1)*C1 (mod 2^64), z ^= z >> 32, z *= C2,
+    z ^= z >> 32; position 8w + q (q < 8) gets ((byte q of z) * K) >> 8
+    (bytes little-endian). Mirrors gen_row (csrc/eval_common.cuh, gen 1)."""
+    W8 = (V + 7) // 8
     c = np.arange(first, first + n, dtype=np.uint64)[:, None]
-    j = np.arange(W, dtype=np.uint64)[None, :]
+    w = np.arange(1, W8 + 1, dtype=np.uint64)[None, :]
     with np.errstate(over="ignore"):
-        ctr = c * np.uint64(W) + j + np.uint64(1)
-        h = splitmix64(np.uint64(seed & M64) + ctr * np.uint64(GOLDEN))
-    out = np.empty((n, 4 * W), np.uint8)
-    for q in range(4):
-        v = (h >> np.uint64(16 * q)) & np.uint64(0xFFFF)
-        out[:, q::4] = ((v * np.uint64(K)) >> np.uint64(16)).astype(np.uint8)
+        h = splitmix64(np.uint64(seed & M64) + (c + np.uint64(1)) * np.uint64(GOLDEN))
+        z = h + w * np.uint64(GEN_C1)
+        z = z ^ (z >> np.uint64(32))
+        z = z * np.uint64(GEN_C2)
+        z = z ^ (z >> np.uint64(32))
+    b = np.ascontiguousarray(z.astype("<u8")).view(np.uint8).reshape(n, 8 * W8)
+    out = ((b.astype(np.uint32) * np.uint32(K)) >> np.uint32(8)).astype(np.uint8)
     return out[:, :V]

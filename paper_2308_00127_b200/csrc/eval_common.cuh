@@ -364,6 +364,13 @@ static __device__ __noinline__ void reduce_best(double bc, hs_i64 bi, Best *part
     }
 }
 
+// four bytes b -> four genes (b * K) >> 8 (K <= 256): even and odd bytes
+// multiplied in 16-bit lanes, the high byte of each lane kept
+__device__ __forceinline__ hs_u32 gen_bytes_to_genes(hs_u32 x, hs_u32 K) {
+    const hs_u32 e = x & 0x00FF00FFu, o = (x >> 8) & 0x00FF00FFu;
+    return (((e * K) >> 8) & 0x00FF00FFu) | ((o * K) & 0xFF00FF00u);
+}
+
 // K6: on-device candidate rows (oracle/hs_oracle.py::gen_genes, or
 // mixed-radix enumeration), expanded over the group map.
 __device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 cidx) {
@@ -397,18 +404,25 @@ __device__ __forceinline__ void gen_row(const EvalParams &a, hs_u8 *r8, hs_i64 c
         return;
     }
     if (a.gen == 1) {
-        const int W4 = (NG + 3) >> 2;
+        // one splitmix64 per candidate, then per 8 genes one 64-bit
+        // multiply-xorshift of h + (w+1) * C; each byte b of it gives the
+        // gene (b * K) >> 8, four at a time in two 16-bit-lane products
+        // (b * K < 2^16 for K <= 256): ~4 instructions per gene where a
+        // splitmix64 per 4 genes cost ~8 (the generator was a quarter of the
+        // generated-candidate evaluation's issue slots)
+        const int W4 = (NG + 3) >> 2, W8 = (W4 + 1) >> 1;
         hs_u32 *row = reinterpret_cast<hs_u32 *>(r8);
-        for (int w = 0; w < W4; ++w) {
-            const hs_u64 ctr = c * (hs_u64)W4 + (hs_u64)w + 1ull;
-            const hs_u64 h = splitmix64(a.seed + ctr * 0x9E3779B97F4A7C15ull);
-            hs_u32 pk = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const hs_u32 v16 = (hs_u32)((h >> (16 * q)) & 0xFFFFull);
-                pk |= ((v16 * (hs_u32)K) >> 16) << (8 * q);
-            }
-            row[w] = pk;
+        const hs_u64 h = splitmix64(a.seed + (c + 1ull) * 0x9E3779B97F4A7C15ull);
+        const hs_u32 Ku = (hs_u32)K;
+        hs_u64 zc = h;
+        for (int w = 0; w < W8; ++w) {
+            zc += 0xD1B54A32D192ED03ull;
+            hs_u64 z = zc ^ (zc >> 32);
+            z *= 0xD6E8FEB86659FD93ull;
+            z ^= z >> 32;
+            const hs_u32 lo = (hs_u32)z, hi = (hs_u32)(z >> 32);
+            row[2 * w] = gen_bytes_to_genes(lo, Ku);
+            if (2 * w + 1 < W4) row[2 * w + 1] = gen_bytes_to_genes(hi, Ku);
         }
     } else if (c < (1ull << 32)) {
         hs_u32 x = (hs_u32)c;
