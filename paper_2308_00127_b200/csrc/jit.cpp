@@ -131,6 +131,9 @@ JitOpts JitOpts::from_env() {
             if (k == "ahead") o.ahead = std::atoi(v.c_str());
             if (k == "fma") o.fma = std::atoi(v.c_str()) != 0;
             if (k == "glanes") o.gslot_lanes = std::max(32, std::atoi(v.c_str()));
+            // end-time slots in the global-memory tier regardless of fit
+            // (normally chosen by jit_build; also for hs_plan_emit_specialized)
+            if (k == "gslots") o.gslots = std::atoi(v.c_str()) != 0;
             if (k == "sync") o.sync = std::atoi(v.c_str());
             if (k == "gword") o.gword = std::atoi(v.c_str()) != 0;
             if (k == "dom") o.dom = std::atoi(v.c_str()) != 0;
@@ -272,7 +275,7 @@ JitLayout jit_layout(const Plan &p, const JitOpts &o, int T, int slots, int ld_c
 int64_t per_lane_bytes(const Plan &p, const JitOpts &o, int slots, int ld_cap,
                        bool dbuf) {
     if (p.batched)  // tiles, [slot][part] end times, device-available times
-        return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 * p.P + 8 * p.K;
+        return (dbuf ? 2 : 1) * ld_cap + int64_t(o.gslots ? 0 : slots) * 8 * p.P + 8 * p.K;
     const bool avail = o.avail_smem || p.K > 4;
     if (o.gslots || o.tmem) slots = 0;
     return (dbuf ? 2 : 1) * ld_cap + int64_t(slots) * 8 + (avail ? 8 * p.K : 0) + (p.mem_check ? 8 * p.K : 0);
@@ -314,21 +317,25 @@ std::string stage(int64_t dst, const char *section, int64_t bytes) {
 // Each term is then one bit test folded into the predicated max. Uniform
 // full-mesh bandwidth only (one om/beta per producer); the parts' end times
 // live in registers for consumers within `near` positions, else in
-// shared-memory slots [slot][part][lane].
+// shared-memory slots [slot][part][lane] -- or, when those leave fewer than
+// 96 lanes per CTA (WS200 at L = 4: ~100 far-read producers x 3 parts -> 64
+// lanes), in the global-memory tier ([slot][part][lane] per CTA, L2-resident,
+// like K1''s).
 bool jit_batched_ok(const Plan &p) {
     if (!(p.batched && p.P <= 4 && p.n_opt <= 255 && p.full_mesh && p.n_classes <= 1 &&
           p.K <= kJitMaxK && !p.nan_possible && p.V > 0 && p.V <= kJitMaxV &&
           p.E <= kJitMaxE))
         return false;
-    // only where the parts' slots leave >= 96 lanes per CTA in shared
-    // memory (WS200 at L = 4: ~100 far-read producers x 3 parts -> 64
-    // lanes, slower than the plan walker's global slot tier)
-    const JitOpts o = JitOpts::from_env();
+    JitOpts o = JitOpts::from_env();
     const int slots = jit_emit_batched(p, 32, o, nullptr, true);
     const int64_t head = head_bytes(p, o);
-    const int64_t lanes = (227 * 1024 - 2048 - head) /
-                          std::max<int64_t>(1, per_lane_bytes(p, o, slots, p.pref_ld() + 16, false));
-    return lanes >= 96;
+    auto lanes = [&](const JitOpts &oo) {
+        return (227 * 1024 - 2048 - head) /
+               std::max<int64_t>(1, per_lane_bytes(p, oo, slots, p.pref_ld() + 16, false));
+    };
+    if (lanes(o) >= 96) return true;
+    o.gslots = true;
+    return lanes(o) >= 96;
 }
 
 namespace {
@@ -403,7 +410,7 @@ int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, b
     }
     if (src == nullptr) return next;
     const int ld_cap = p.pref_ld() + 16;
-    const BatLayout l = bat_layout(p, T, next, ld_cap, dbuf);
+    const BatLayout l = bat_layout(p, T, o.gslots ? 0 : next, ld_cap, dbuf);
     // the option tables
     std::vector<uint64_t> opt(NO, 0);
     for (int oo = 0; oo < NO; ++oo)
@@ -443,8 +450,13 @@ int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, b
     s += "template <bool TRACE, bool SYNC>\n__device__ __forceinline__ void jit_body(hs_u8 *smem, "
          "const hs_u8 *g, int li, hs_i64 cand, bool valid, int gene_bad, double *starts, "
          "double &ms_out, int &st_out, double *EG, hs_u32 TB, const double *DG) {\n";
-    s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
-         ") + li;\n    (void)E; (void)EG; (void)TB; (void)DG;\n";
+    // parts' end-time slots [slot][part][lane]: shared memory, or this
+    // CTA's region of the global-memory tier
+    if (o.gslots)
+        s += "    double *E = EG + li;\n    (void)E; (void)TB; (void)DG;\n";
+    else
+        s += "    double *E = reinterpret_cast<double *>(smem + " + std::to_string(l.ends) +
+             ") + li;\n    (void)E; (void)EG; (void)TB; (void)DG;\n";
     s += "    const hs_u16 *OVD = reinterpret_cast<const hs_u16 *>(smem + " +
          std::to_string(l.ovd) + ");\n";
     s += "    const unsigned long long *OPT = reinterpret_cast<const unsigned long long *>(smem + " +
@@ -541,7 +553,8 @@ int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, b
     s += stage(l.bd, "bdur", int64_t(V) * NO * P * 8);
     if (l.bok_on) s += stage(l.bok, "bdur_ok", int64_t(V) * NO * P);
     s += "  JitBody<TRACE> body;\n  body.smem = smem;\n  body.starts = a.starts;\n"
-         "  body.eg = nullptr;\n  body.tb = 0u;\n  body.dg = nullptr;\n"
+         "  body.eg = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
+         "  body.tb = 0u;\n  body.dg = nullptr;\n"
          "  eval_tiles(a, smem, body);\n}\n";
     std::snprintf(buf, sizeof buf,
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
@@ -1289,6 +1302,21 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     // too few lanes with the end times in shared memory: move them to the
     // global-memory tier ([slot][lane] per CTA, L2-resident; `gslot_lanes`
     // bounds the footprint SMs x lanes x slots x 8 B)
+    if (p.batched && T < 96 && slots > 0) {
+        // K8': the parts' slots to the global-memory tier (jit_batched_ok)
+        JitOpts og = ob;
+        og.gslots = true;
+        auto lanes_g = [&](bool db) {
+            return int(std::min<int64_t>(budget / per_lane_bytes(p, og, slots, ld_cap, db),
+                                         std::min(o.lanes, o.gslot_lanes)) / 32 * 32);
+        };
+        const bool dg = lanes_g(true) >= lanes_g(false);
+        if (lanes_g(dg) > T) {
+            oe.gslots = true;
+            dbuf = dg;
+            T = lanes_g(dg);
+        }
+    }
     if (T < 128 && slots > 0 && !p.batched) {
         JitOpts og = ob;
         og.gslots = true;
@@ -1406,7 +1434,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->ends_global = oe.gslots;
     m->tmem = oe.tmem;
     if (p.batched) {
-        const BatLayout l = bat_layout(p, T, n_slots, ld_cap, dbuf);
+        const BatLayout l = bat_layout(p, T, oe.gslots ? 0 : n_slots, ld_cap, dbuf);
         m->smem_tile = l.tile;
         m->smem_tile2 = l.tile2;
         m->smem_ends = l.ends;
