@@ -556,12 +556,13 @@ int jit_emit_batched(const Plan &p, int T, const JitOpts &o, std::string *src, b
          "  body.eg = a.ends_g ? a.ends_g + blockIdx.x * a.ends_g_cta : nullptr;\n"
          "  body.tb = 0u;\n  body.dg = nullptr;\n"
          "  eval_tiles(a, smem, body);\n}\n";
+    // o.ctas: the CTAs per SM jit_build sized the shared memory for
     std::snprintf(buf, sizeof buf,
-                  "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
+                  "extern \"C\" __global__ void __launch_bounds__(%d, %d) "
                   "hs_jit_eval(const EvalParams a) { jit_main<false>(a); }\n"
                   "extern \"C\" __global__ void __launch_bounds__(%d, 1) "
                   "hs_jit_trace(const EvalParams a) { jit_main<true>(a); }\n",
-                  T, T);
+                  T, std::max(1, o.ctas), T);
     s += buf;
     return next;
 }
@@ -1379,6 +1380,39 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
     }
+    if (p.batched && !o.lanes_set) {
+        // K8': lanes per SM, not per CTA, is what hides latency. A CTA
+        // whose tables + tiles take more than half of the SM's shared memory
+        // leaves it at one CTA (Inception-v3 at L = 4: 140 KB -> 256 lanes
+        // per SM where ResNet-50's 114 KB CTAs run two): search the lane
+        // count and tile double-buffering for the most resident lanes per SM
+        // (ties: the larger CTA, then double-buffered)
+        int smem_sm = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const int ns = oe.gslots ? 0 : slots;
+        auto per_sm = [&](int t, bool db, int *ctas) {
+            const int64_t sm = bat_layout(p, t, ns, ld_cap, db).total;
+            if (sm > optin - 1024) return 0;
+            *ctas = int(std::min<int64_t>({int64_t(2048 / t), int64_t(smem_sm) / (sm + 1024), 4}));
+            // the global slot tier's L2 footprint grows with the lanes per SM
+            if (oe.gslots) *ctas = std::min(*ctas, std::max(1, o.gslot_lanes / t));
+            return t * *ctas;
+        };
+        int c0 = 1;
+        int best = per_sm(T, dbuf, &c0), bctas = c0;
+        for (int db = 1; db >= 0; --db)
+            for (int t = std::min(o.lanes, 512) / 32 * 32; t >= 64; t -= 32) {
+                int c = 1;
+                const int l = per_sm(t, db != 0, &c);
+                if (l > best) {
+                    best = l;
+                    T = t;
+                    dbuf = db != 0;
+                    bctas = c;
+                }
+            }
+        oe.ctas = std::max(1, bctas);
+    }
     std::string src;
     oe.dbuf = dbuf;
     if (p.batched)
@@ -1493,6 +1527,8 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     m->blocks_per_sm = std::max(1, std::min(2048 / T, int(smem_sm / (m->smem + 1024))));
     // each CTA allocates 512 / tm_ctas TMEM columns
     if (m->tmem) m->blocks_per_sm = std::min(m->blocks_per_sm, oe.tm_ctas);
+    // K8': the CTAs per SM the lane search sized it for (launch bounds, L2)
+    if (p.batched) m->blocks_per_sm = std::min(m->blocks_per_sm, std::max(1, oe.ctas));
     m->sms = sms;
     m->src_bytes = src.size();
     m->compile_ms = std::chrono::duration<double, std::milli>(

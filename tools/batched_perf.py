@@ -3,7 +3,7 @@
 throughput objective, L in {2, 4, 8}: explicit random extended genomes and
 on-device generated ones.
 
-    python tools/batched_perf.py rn50f iv3f
+    python tools/batched_perf.py rn50f iv3f      (QP_L=4 for one L)
 """
 import json
 import os
@@ -22,7 +22,7 @@ for name in sys.argv[1:] or ["rn50f"]:
     with open(f"tests/golden/instances/{name}.json") as f:
         doc = json.load(f)
     g, hw, t = hs.load_instance(doc)
-    for L in (2, 4, 8):
+    for L in [int(x) for x in os.environ.get("QP_L", "2,4,8").split(",")]:
         try:
             plan = _plan(g, hw, t, L, None)
         except Exception as exc:  # noqa: BLE001

@@ -55,7 +55,7 @@ if has sanitize; then
       > gpurun_out/${T}_sanitize_${tool}.log 2>&1
     echo "sanitize $tool rc=$?"
   done
-  timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/sanitize_run.py jit trace aot batched bounds validate \
+  timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/sanitize_run.py jit trace aot batched batched_jit gen bounds validate \
     > gpurun_out/${T}_sanitize_synccheck.log 2>&1; echo "synccheck rc=$?"
   timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/sanitize_run.py sa_only \
     > gpurun_out/${T}_sanitize_synccheck_sa.log 2>&1; echo "synccheck sa rc=$?"

@@ -44,8 +44,8 @@ def check(name, n, jit):
     return g, hw, t
 
 
-which = sys.argv[1:] or ["jit", "trace", "search", "aot", "batched", "bounds",
-                         "validate"]
+which = sys.argv[1:] or ["jit", "trace", "search", "aot", "batched", "batched_jit",
+                         "gen", "bounds", "validate"]
 if "jit" in which:
     check("ws200", 148 * 384 + 1000, True)
 if "trace" in which:
@@ -87,6 +87,39 @@ if "batched" in which:
                                               dtype=np.uint8)
     ms = hs.fitness_batched(torch.from_numpy(genes).cuda(), g, hw, t, 4)
     print("batched ok", float(ms.min()))
+if "batched_jit" in which:
+    # specialised K8 on its global-memory slot tier (WS200, L = 4) against
+    # the plan walker
+    from paper_2308_00127_b200.plan import Plan
+    g, hw, t = hs.load_instance(doc("ws200"))
+    nopt = len(hs.batched_options(g, hw, t, 4))
+    jit, aot = Plan(g, hw, t, 4, batched=()), Plan(g, hw, t, 4, batched=())
+    jit.specialize()
+    n = 2 * 148 * 192 + 77
+    genes = torch.randint(0, nopt, (n, jit.pref_ld), dtype=torch.uint8, device="cuda")
+    m1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    m2 = torch.empty_like(m1)
+    jit.eval(genes, m1)
+    aot.eval(genes, m2)
+    assert torch.equal(m1.view(torch.int64), m2.view(torch.int64))
+    print("batched_jit ok", float(m1.min()))
+if "gen" in which:
+    # hash-random generated rows (no gene check pass) through the
+    # specialised evaluator, re-derived and re-scored by the oracle
+    from paper_2308_00127_b200 import _native as N
+    d = doc("ws200")
+    g, hw, t = hs.load_instance(d)
+    plan = get_plan(g, hw, t, 1)
+    plan.specialize()
+    n = 148 * 384 + 1000
+    ms = torch.empty(n, dtype=torch.float64, device="cuda")
+    out = torch.empty((n, plan.V), dtype=torch.uint8, device="cuda")
+    plan.eval_gen(N.GEN_RANDOM, 11, 5, n, makespan=ms, genes_out=out)
+    want_g = O.gen_genes(11, 5, n, plan.V, plan.K)
+    assert np.array_equal(out.cpu().numpy(), want_g)
+    want, _ = O.fitness_np(O.build_tables(O.Instance.from_doc(d), 1), want_g[:4000])
+    assert np.array_equal(ms.cpu().numpy()[:4000].view(np.uint64), want.view(np.uint64))
+    print("gen ok")
 if "bounds" in which:
     g, hw, t = hs.load_instance(doc("ws_stack_10x20"))
     d = hs.k_edge_components(g, 1)
