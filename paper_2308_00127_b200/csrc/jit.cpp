@@ -1303,8 +1303,19 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     // too few lanes with the end times in shared memory: move them to the
     // global-memory tier ([slot][lane] per CTA, L2-resident; `gslot_lanes`
     // bounds the footprint SMs x lanes x slots x 8 B)
-    if (p.batched && T < 96 && slots > 0) {
-        // K8': the parts' slots to the global-memory tier (jit_batched_ok)
+    int smem_sm_all = 0;
+    cudaDeviceGetAttribute(&smem_sm_all, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    const int64_t smem_lanes_sm =
+        p.batched && slots > 0
+            ? int64_t(T) * std::max<int64_t>(1, smem_sm_all /
+                                                   (bat_layout(p, std::max(T, 32), slots, ld_cap,
+                                                               dbuf).total + 1024))
+            : 0;
+    if (p.batched && slots > 0 && smem_lanes_sm < o.gslot_lanes) {
+        // K8': the parts' slots to the global-memory tier when shared
+        // memory holds fewer lanes per SM than that tier runs (r4e, WS200:
+        // L = 2 109 lanes in shared memory 2.5e8 -> 192 lanes 5.9e8 cand/s;
+        // jit_batched_ok)
         JitOpts og = ob;
         og.gslots = true;
         auto lanes_g = [&](bool db) {
