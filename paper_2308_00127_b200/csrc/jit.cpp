@@ -1391,7 +1391,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
         if (err) *err = "graph too large for the specialised evaluator";
         return HS_EINVAL;
     }
-    if (p.batched && !o.lanes_set) {
+    if (p.batched) {
         // K8': lanes per SM, not per CTA, is what hides latency. A CTA
         // whose tables + tiles take more than half of the SM's shared memory
         // leaves it at one CTA (Inception-v3 at L = 4: 140 KB -> 256 lanes
@@ -1401,17 +1401,23 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
         int smem_sm = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
         const int ns = oe.gslots ? 0 : slots;
+        // at most two CTAs per SM: three single-buffered 224-lane CTAs
+        // (672 lanes, 97 registers) ran ResNet-50 at L = 4 at 1.5e9 where
+        // two double-buffered 256-lane CTAs run 2.2e9 (r4g vs r4c)
         auto per_sm = [&](int t, bool db, int *ctas) {
             const int64_t sm = bat_layout(p, t, ns, ld_cap, db).total;
             if (sm > optin - 1024) return 0;
-            *ctas = int(std::min<int64_t>({int64_t(2048 / t), int64_t(smem_sm) / (sm + 1024), 4}));
+            *ctas = int(std::min<int64_t>({int64_t(2048 / t), int64_t(smem_sm) / (sm + 1024), 2}));
             // the global slot tier's L2 footprint grows with the lanes per SM
             if (oe.gslots) *ctas = std::min(*ctas, std::max(1, o.gslot_lanes / t));
             return t * *ctas;
         };
         int c0 = 1;
-        int best = per_sm(T, dbuf, &c0), bctas = c0;
-        for (int db = 1; db >= 0; --db)
+        int best = per_sm(T, dbuf, &c0), bctas = 0;
+        // only where the default configuration leaves one CTA per SM (and
+        // not under HS_JIT_OPTS=lanes=N): elsewhere it stays as shared
+        // memory allows (ResNet-50 at L = 2: three 256-lane CTAs)
+        for (int db = 1; db >= 0 && c0 < 2 && !o.lanes_set; --db)
             for (int t = std::min(o.lanes, 512) / 32 * 32; t >= 64; t -= 32) {
                 int c = 1;
                 const int l = per_sm(t, db != 0, &c);
@@ -1422,7 +1428,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
                     bctas = c;
                 }
             }
-        oe.ctas = std::max(1, bctas);
+        if (bctas > 0) oe.ctas = bctas;  // the searched configuration
     }
     std::string src;
     oe.dbuf = dbuf;
@@ -1539,7 +1545,7 @@ int jit_build(const Plan &p, int device, JitModule **out, std::string *err) {
     // each CTA allocates 512 / tm_ctas TMEM columns
     if (m->tmem) m->blocks_per_sm = std::min(m->blocks_per_sm, oe.tm_ctas);
     // K8': the CTAs per SM the lane search sized it for (launch bounds, L2)
-    if (p.batched) m->blocks_per_sm = std::min(m->blocks_per_sm, std::max(1, oe.ctas));
+    if (p.batched && oe.ctas > 1) m->blocks_per_sm = std::min(m->blocks_per_sm, oe.ctas);
     m->sms = sms;
     m->src_bytes = src.size();
     m->compile_ms = std::chrono::duration<double, std::milli>(
