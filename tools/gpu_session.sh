@@ -11,7 +11,10 @@
 #   ncu       ncu --set full of the bench's own hs_jit_eval launch (+ raw /
 #             details CSV, tools/ncu_summary.py) and the launch list of the
 #             bench command (--metrics gpu__time_duration.sum)
-#   sanitize  compute-sanitizer memcheck / racecheck / synccheck over
+#   sanitize  (refused on the current GPU pool since round 2's r4g: runs
+#             under compute-sanitizer had left GPUs needing a reset; use
+#             `python tools/sanitize_run.py` alone for its oracle checks)
+#             compute-sanitizer memcheck / racecheck / synccheck over
 #             tools/sanitize_run.py (synccheck of hs_jit_sa in its own
 #             process: profiles/README.md r2c)
 #   sweep     tools/jit_sweep.sh (OPTS, WL)
