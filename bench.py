@@ -587,6 +587,9 @@ def search_tts(names=("ws_stack_10x20", "ws200", "tf96"), budget=2000,
     # one launch; chain c equals the single run at seed c
     for name in names:
         g, hw, t = hs.load_instance(_inst(name))
+        # the graph-specialised body, like the single-chain runs above (a
+        # freshly loaded instance is a new plan)
+        hs.specialize(g, hw, t, 1)
         for algo in ("sa", "ea"):
             fn = hs.simulated_annealing_multi if algo == "sa" else \
                 hs.one_plus_one_ea_multi
