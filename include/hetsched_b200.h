@@ -50,6 +50,8 @@ extern "C" {
 #define HS_ECYCLE 2   /* -> GraphError("cycle detected"), core.py:94-95   */
 #define HS_ECUDA 3    /* -> RuntimeError                                   */
 #define HS_ENOMEM 4   /* -> MemoryError                                    */
+#define HS_EHOST 5    /* case left to the host restatement, which raises the
+                         reference's exception (hs_plan_greedy)            */
 
 /* per-candidate status (hs_eval*, hs_trace) */
 #define HS_ST_OK 0        /* feasible: makespan finite or +inf by latency */
@@ -134,6 +136,17 @@ int hs_plan_create_batched(const hs_instance_desc *desc, const int32_t *splits,
 int hs_plan_batched_options(const hs_plan *plan, int32_t *n_opt,
                             int32_t *max_parts, int32_t *table);
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info);
+
+/* greedy (heuristics.py:192-210, replaces _ListScheduler-driven greedy for
+ * SA's start): BFS order, each task on the sorted-order device whose
+ * placement grows the partial makespan least (by more than 1e-12), with
+ * try_place's checks (heuristics.py:86-124). Host only, no CUDA. genes[V]
+ * = sorted-device index per BFS position, starts[V] (may be NULL),
+ * *makespan. HS_EHOST when the cost model can produce NaN, a reached
+ * latency entry is missing or a task has no feasible device: the caller's
+ * host scheduler then raises the reference's exception. */
+int hs_plan_greedy(const hs_plan *plan, uint8_t *genes, double *starts,
+                   double *makespan);
 /* Specialise the evaluator to this plan on the current device: the plan is
  * emitted as straight-line CUDA (predecessor slots, communication and
  * latency constants baked in) and compiled by NVRTC for sm_100a (one-time

@@ -15,7 +15,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhetsched_b200.so")
 
-HS_OK, HS_EINVAL, HS_ECYCLE, HS_ECUDA, HS_ENOMEM = 0, 1, 2, 3, 4
+HS_OK, HS_EINVAL, HS_ECYCLE, HS_ECUDA, HS_ENOMEM, HS_EHOST = 0, 1, 2, 3, 4, 5
 ST_OK, ST_BATCH, ST_MEMORY, ST_LINK, ST_MISSING, ST_GENE = 0, 1, 2, 3, 4, 5
 
 GEN_RANDOM, GEN_ENUM, GEN_NEIGHBOR = 1, 2, 3
@@ -86,6 +86,7 @@ def load() -> C.CDLL:
             "hs_plan_batched_options": (C.c_int, [vp, vp, vp, vp]),
             "hs_plan_get_info": (C.c_int, [vp, _p(PlanInfo)]),
             "hs_plan_order": (C.c_int, [vp, vp, vp]),
+            "hs_plan_greedy": (C.c_int, [vp, vp, vp, _p(C.c_double)]),
             "hs_plan_specialize": (C.c_int, [vp, _p(C.c_double)]),
             "hs_plan_emit_specialized": (C.c_int, [vp, i32, vp, i64,
                                                    _p(C.c_int64)]),
@@ -149,6 +150,7 @@ def exported_symbols() -> list[str]:
             "hs_plan_create",
             "hs_plan_destroy", "hs_plan_create_batched",
             "hs_plan_batched_options", "hs_plan_get_info", "hs_plan_order",
+            "hs_plan_greedy",
             "hs_plan_specialize", "hs_plan_emit_specialized", "hs_eval",
             "hs_eval_host", "hs_eval_host_packs", "hs_pack_genes2", "hs_eval_packed", "hs_eval_host_packed",
             "hs_eval_packed3", "hs_eval_host_packed3", "hs_ea_run",

@@ -658,6 +658,77 @@ int hs_plan_emit_specialized(const hs_plan *plan, int32_t lanes, char *buf,
     return HS_OK;
 }
 
+int hs_plan_greedy(const hs_plan *plan, uint8_t *genes, double *starts, double *makespan) {
+    // greedy (heuristics.py:192-210) over the plan's tables: BFS order, each
+    // task on the device (sorted order) whose placement grows the partial
+    // makespan least by more than 1e-12; try_place's checks in its order
+    // (batch size, memory, links, then the latency entry)
+    if (!plan || !genes) return set_err(HS_EINVAL, "null argument");
+    const hs::Plan &p = plan->p;
+    if (p.batched) return set_err(HS_EINVAL, "greedy needs a non-batched plan");
+    // NaN comparisons, missing latency entries and infeasible tasks are left
+    // to the Python scheduler, which raises the reference's exceptions
+    if (p.nan_possible) return set_err(HS_EHOST, "greedy: NaN in the cost model");
+    const int V = p.V, K = p.K;
+    std::vector<double> avail(size_t(K), 0.0), mem(size_t(K), 0.0), endt(size_t(V), 0.0);
+    double ms = 0.0;
+    auto cls_of = [&](int u, int v) {
+        const size_t at = 2 * (size_t(u) * K + v);
+        return int(p.bclass[at]) | (int(p.bclass[at + 1]) << 8);
+    };
+    for (int i = 0; i < V; ++i) {
+        const hs::NodeRec &nr = p.nodes[i];
+        const double ex = p.extra[i];
+        int bk = -1;
+        double bc = 0.0, bs = 0.0, be = 0.0;
+        for (int k = 0; k < K; ++k) {
+            if (!p.okL[k]) continue;
+            if (mem[k] + ex > p.cap[k]) continue;
+            double ready = 0.0;
+            bool nolink = false;
+            for (int e = nr.e_begin; e < nr.e_end; ++e) {
+                const hs::EdgeRec &er = p.edges[e];
+                const int src = genes[er.gpos];
+                double c;
+                if (p.uniform_comm) {
+                    c = src == k ? 0.0 : er.c;
+                } else {
+                    const int cl = cls_of(src, k);
+                    if (cl == 0xFFFF) {
+                        nolink = true;
+                        break;
+                    }
+                    c = p.ctab[size_t(er.crow) + cl];
+                }
+                const double x = endt[er.gpos] + c;
+                if (x > ready) ready = x;
+            }
+            if (nolink) continue;
+            if (!p.dur_ok[size_t(i) * K + k])
+                return set_err(HS_EHOST, "greedy: missing latency entry");
+            const double a = avail[k];
+            const double st = a > ready ? a : ready;
+            const double en = st + p.dur[size_t(i) * K + k];
+            const double cand = en > ms ? en : ms;
+            if (bk < 0 || cand < bc - 1e-12) {
+                bk = k;
+                bc = cand;
+                bs = st;
+                be = en;
+            }
+        }
+        if (bk < 0) return set_err(HS_EHOST, "greedy: no feasible placement");
+        avail[bk] = be;
+        mem[bk] += ex;
+        endt[i] = be;
+        genes[i] = uint8_t(bk);
+        if (starts) starts[i] = bs;
+        if (be > ms) ms = be;
+    }
+    if (makespan) *makespan = ms;
+    return HS_OK;
+}
+
 int hs_plan_get_info(const hs_plan *plan, hs_plan_info *info) {
     if (!plan || !info) return set_err(HS_EINVAL, "null argument");
     const hs::Plan &p = plan->p;

@@ -481,9 +481,58 @@ class _HostScheduler:
             self.makespan = end
 
 
+def _greedy_native(g, hw, table, L: int):
+    """(plan, genes uint8 [V], starts [V], makespan) of greedy from the
+    native scheduler over the plan's tables (hs_plan_greedy), or None when
+    the case is left to the host scheduler (NaN-capable cost model, missing
+    latency entry, infeasible task: it raises the reference's exception)."""
+    import ctypes as C
+    if not g.tasks:
+        return None
+    try:
+        plan = get_plan(g, hw, table, L)
+    except (GraphError, ValueError):
+        return None  # the host path raises the reference's error
+    genes = np.empty(plan.V, np.uint8)
+    starts = np.empty(plan.V, np.float64)
+    ms = C.c_double(0.0)
+    rc = N.load().hs_plan_greedy(plan.handle, genes.ctypes.data,
+                                 starts.ctypes.data, C.byref(ms))
+    if rc == N.HS_EHOST:
+        return None
+    N.check(rc, "hs_plan_greedy")
+    return plan, genes, starts, ms.value
+
+
+def _greedy_genome(g, hw, table, L: int) -> MappingGenome:
+    """SA's start genome: greedy's mapping in BFS positions."""
+    r = _greedy_native(g, hw, table, L)
+    if r is None:
+        start = greedy(g, hw, table, L)
+        return genome_from_map(g, hw, {b.task: b.device for b in start.batches})
+    plan, genes, _, _ = r
+    return MappingGenome(genes=tuple(genes.tolist()), order=tuple(plan.order))
+
+
 def greedy(g, hw, table, L: int) -> Schedule:
     """BFS order, each task where the partial makespan grows least
-    (heuristics.py:192-210)."""
+    (heuristics.py:192-210): the native scheduler (hs_plan_greedy), the host
+    restatement below for the cases it leaves to the host."""
+    r = _greedy_native(g, hw, table, L)
+    if r is not None:
+        plan, genes, starts, ms = r
+        devs = sorted(hw.devices)
+        inputs = tuple(range(1, L + 1))
+        return Schedule(batches=tuple(
+            ScheduledBatch(task=t, device=devs[k], size=L, inputs=inputs,
+                           start=x)
+            for t, k, x in zip(plan.order, genes.tolist(), starts.tolist())),
+            objective=ms, input_count=L)
+    return _greedy_host(g, hw, table, L)
+
+
+def _greedy_host(g, hw, table, L: int) -> Schedule:
+    """Host restatement of greedy (heuristics.py:192-210)."""
     ls = _HostScheduler(g, hw, table, L)
     devs = sorted(hw.devices)
     for task in bfs_topological_order(g):
@@ -601,9 +650,7 @@ def simulated_annealing(g, hw, table, L: int, seed: int = 0,
     launch (K10, hs_sa_run) with numpy's PCG64 restated on the device.
     """
     gen = np.random.default_rng(seed)
-    start = greedy(g, hw, table, L)
-    mapping = {b.task: b.device for b in start.batches}
-    cur = genome_from_map(g, hw, mapping)
+    cur = _greedy_genome(g, hw, table, L)
     cur_fit = fitness(cur, g, hw, table, L)
     best, best_fit = cur, cur_fit
     temp = max(t0_fraction * cur_fit, 1e-9)
@@ -790,8 +837,7 @@ def simulated_annealing_multi(g, hw, table, L: int, seeds: Sequence[int],
     seeds = [int(s) for s in seeds]
     if not seeds:
         return []
-    start = greedy(g, hw, table, L)
-    cur = genome_from_map(g, hw, {b.task: b.device for b in start.batches})
+    cur = _greedy_genome(g, hw, table, L)
     cur_fit = fitness(cur, g, hw, table, L)
     V = len(cur.genes)
     if V == 0 or budget <= 0:

@@ -209,3 +209,51 @@ def test_host_packer_back_to_back_jobs():
         hs.pack_genes(np.full((2, 9), 4, np.uint8))
     with pytest.raises(hs.GraphError):
         hs.pack_genes(np.full((2, 9), 256, np.int64))
+
+
+def test_native_greedy_equals_host_greedy():
+    """hs_plan_greedy (SA's start, greedy()) equals the host restatement of
+    greedy (heuristics.py:192-210) -- mapping, every start and the
+    objective, bit for bit -- on every golden instance (L = 1, and 2 / 4 on
+    the CNNs), the random fixtures (missing links, tight memory, L > 1) and
+    the reference's recorded greedy runs; cases it leaves to the host
+    (HS_EHOST) raise the same exception through greedy()."""
+    import json as _json
+    from paper_2308_00127_b200.heuristics import (_greedy_host,
+                                                  _greedy_native)
+    cases = [(instance_doc(n), 1) for n in INSTANCES]
+    cases += [(instance_doc(n), L) for n in ("rn50f", "iv3f") for L in (2, 4)]
+    cases += [(d, d.get("L", 1)) for d in random_docs()]
+    native = host_only = 0
+    for doc, L in cases:
+        g, hw, t = hs.load_instance(doc)
+        try:
+            want = _greedy_host(g, hw, t, L)
+        except Exception as exc:  # noqa: BLE001
+            with pytest.raises(type(exc)):
+                hs.greedy(g, hw, t, L)
+            host_only += 1
+            continue
+        r = _greedy_native(g, hw, t, L)
+        if r is None:
+            host_only += 1
+        else:
+            native += 1
+        got = hs.greedy(g, hw, t, L)
+        assert got == want
+        assert [b.start for b in got.batches] == [b.start for b in want.batches]
+    assert native >= len(INSTANCES)
+    path = os.path.join(ROOT, "tests", "golden", "heuristics.json")
+    with open(path) as f:
+        entries = _json.load(f)
+    for e in entries:
+        res = e["greedy"]
+        g, hw, t = hs.load_instance(e)
+        if "error" in res:
+            with pytest.raises(hs.ScheduleError):
+                hs.greedy(g, hw, t, e["L"])
+            continue
+        s = hs.greedy(g, hw, t, e["L"])
+        assert s.objective.hex() == res["objective"] or \
+            float.fromhex(res["objective"]) == s.objective
+        assert {b.task: b.device for b in s.batches} == res["mapping"]
