@@ -1020,11 +1020,16 @@ def one_plus_one_ea_multi(g, hw, table, L: int, seeds: Sequence[int],
     rows = np.zeros((C, stride), np.uint8)
     states = []
     if biased:
-        start = genome_from_map(g, hw, {b.task: b.device for b in
-                                        met(g, hw, table, L).batches})
+        start = genome_from_map(g, hw, _met_mapping(g, hw, table, L))
+        ms0, st0 = _eval_rows(get_plan(g, hw, table, L, start.order),
+                              np.asarray(start.genes, np.uint8)[None, :])
+        _raise_status(int(st0[0]))
+        if int(st0[0]) != N.ST_OK:  # as met() raises
+            raise ScheduleError("MET mapping infeasible (missing links or memory)")
         rows[:, :V] = np.asarray(start.genes, np.uint8)
-        fits = np.full(C, fitness(start, g, hw, table, L))
-        states = [_gen_words(np.random.default_rng(s)) for s in seeds]
+        fits = np.full(C, float(ms0[0]))
+        # default_rng(s)'s state without a Generator per seed
+        states = [_pcg_words(s) for s in seeds]
     else:
         for c, s in enumerate(seeds):
             gen = np.random.default_rng(s)
@@ -1069,14 +1074,25 @@ def one_plus_one_ea(g, hw, table, L: int, seed: int = 0, budget: int = 2000,
     order = tuple(bfs_topological_order(g))
     n_dev = len(hw.devices)
     V = len(order)
-    if biased:
-        cur = genome_from_map(g, hw, {b.task: b.device for b in
-                                      met(g, hw, table, L).batches})
+    if biased and V:
+        # met()'s mapping and its feasibility from one evaluation (met()
+        # itself traces and builds the Schedule, which the start discards)
+        cur = genome_from_map(g, hw, _met_mapping(g, hw, table, L))
+        ms0, st0 = _eval_rows(get_plan(g, hw, table, L, cur.order),
+                              np.asarray(cur.genes, np.uint8)[None, :])
+        _raise_status(int(st0[0]))
+        if int(st0[0]) != N.ST_OK:
+            raise ScheduleError("MET mapping infeasible (missing links or memory)")
+        cur_fit = float(ms0[0])
     else:
-        cur = MappingGenome(
-            genes=tuple(int(v) for v in gen.integers(n_dev, size=V)),
-            order=order)
-    cur_fit = fitness(cur, g, hw, table, L)
+        if biased:
+            cur = genome_from_map(g, hw, {b.task: b.device for b in
+                                          met(g, hw, table, L).batches})
+        else:
+            cur = MappingGenome(
+                genes=tuple(int(v) for v in gen.integers(n_dev, size=V)),
+                order=order)
+        cur_fit = fitness(cur, g, hw, table, L)
     p = 1.0 / max(V, 1)
     genes = np.array(cur.genes, np.uint8)
     plan = get_plan(g, hw, table, L) if V else None
