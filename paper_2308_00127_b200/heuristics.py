@@ -173,13 +173,14 @@ def decode(genome: MappingGenome, g, hw, table, L: int) -> Optional[Schedule]:
     _raise_status(s)
     if s != N.ST_OK:
         return None
-    inputs = tuple(range(1, L + 1))
-    devs = sorted(hw.devices)
-    batches = tuple(
-        ScheduledBatch(task=t, device=devs[genome.genes[i]], size=L,
-                       inputs=inputs, start=float(starts[0, i]))
-        for i, t in enumerate(genome.order))
-    return Schedule(batches=batches, objective=float(ms[0]), input_count=L)
+    # the batch tuple is built on first access (_LazySchedule: a search
+    # that returns decode()'s Schedule pays for its V ScheduledBatch objects
+    # only when a caller reads them)
+    return _LazySchedule(
+        objective=float(ms[0]), input_count=L,
+        lazy=(tuple(genome.order), tuple(sorted(hw.devices)),
+              [int(k) for k in genome.genes], starts[0].tolist(), L,
+              tuple(range(1, L + 1))))
 
 
 def fitness(genome: MappingGenome, g, hw, table, L: int) -> float:
